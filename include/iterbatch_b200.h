@@ -1,0 +1,152 @@
+/*
+ * iterbatch_b200.h — C ABI of the B200-native iteration-batching runtime.
+ *
+ * Drop-in boundary for the reference's solver API (Python, pkg/src/iterbatch/workloads.py).
+ * The reference has no FFI: its plugin point is the step protocol
+ *   step(state, workers) -> state                       (workloads.py:97,167,325,358)
+ * driven by
+ *   run_loop(program, state, total_iterations)          (workloads.py:442-450, Listing 1)
+ *   run_batched(program, state, batch_size, num_batches)(workloads.py:453-471, Listings 2/3)
+ *   time_workload(program, state, plan, order, repeats) (workloads.py:479-505)
+ *   state_checksum(state)                               (workloads.py:508-525)
+ * This library replaces the body of those calls with a per-RUN boundary (not per step):
+ * upload once, launch N kernels (stream mode) or I graph launches of a K-iteration unrolled
+ * CUDA graph (graph mode), download once. The Python mirror in
+ * paper_2501_09398_b200/workloads.py binds these entry points with ctypes; see INTEGRATION.md.
+ *
+ * Conventions: every int-returning call returns IB_OK (0) or a negative IB_E* status; the
+ * message for the last failure on the calling thread is ib_last_error(). No torch types,
+ * plain pointers and sizes only. One context = one solver instance; not thread-safe.
+ */
+#ifndef ITERBATCH_B200_H
+#define ITERBATCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IB_ABI_VERSION 1
+
+/* status codes (the Python shim maps them to the reference's exception types) */
+#define IB_OK 0
+#define IB_EINVAL (-1)  /* bad argument            -> ValueError   (workloads.py:444-446,463-466) */
+#define IB_ECUDA (-2)   /* CUDA runtime failure    -> RuntimeError */
+#define IB_ENOMEM (-3)  /* device/host allocation  -> MemoryError  */
+#define IB_ESTATE (-4)  /* call out of order (run before build, ...) -> RuntimeError */
+#define IB_ENODEV (-5)  /* no CUDA device          -> RuntimeError (never a CPU fallback) */
+
+/* solver families: one per reference step program (workloads.py:429-439, cli.py:202-207) */
+#define IB_SOLVER_VECTOR 0    /* vector_scale_step  workloads.py:97-105  ; 1 kernel / iteration */
+#define IB_SOLVER_HOTSPOT2D 1 /* hotspot_step 2-D   workloads.py:180-185 ; 1 kernel / iteration */
+#define IB_SOLVER_HOTSPOT3D 2 /* hotspot_step 3-D   workloads.py:186-204 ; 1 kernel / iteration */
+#define IB_SOLVER_FDTD 3      /* fdtd_h_step + fdtd_e_step workloads.py:325-413 ; 2 kernels / it. */
+
+/* arithmetic type of the device state */
+#define IB_F32 0
+#define IB_F64 1
+
+/* graph construction (stream capture vs manual creation) */
+#define IB_BUILD_MANUAL 0  /* cudaGraphCreate + cudaGraphAddKernelNode chain (Listing 3) */
+#define IB_BUILD_CAPTURE 1 /* cudaStreamBeginCapture over the stream-mode launch sequence */
+
+/* flags for ib_graph_build / ib_run_stream */
+#define IB_FLAG_PDL 0x1           /* programmatic dependent launch edges between consecutive kernels */
+#define IB_FLAG_DEVICE_LAUNCH 0x2 /* instantiate with cudaGraphInstantiateFlagDeviceLaunch (Listing 3) */
+#define IB_FLAG_NO_UPLOAD 0x4     /* skip cudaGraphUpload (first launch pays the upload) */
+#define IB_FLAG_WHILE 0x8         /* wrap the K-chain in a conditional WHILE node: one cudaGraphLaunch
+                                     runs all num_batches batches (device-side loop, no host gap) */
+
+/* Per-call timing record. Host times are steady-clock seconds; gpu_s is CUDA-event time on the
+ * context's launch stream (first launch .. end of last kernel). */
+typedef struct ib_times {
+  double create_s;      /* graph create + node add (or capture) */
+  double instantiate_s; /* cudaGraphInstantiate */
+  double upload_s;      /* cudaGraphUpload + sync */
+  double build_s;       /* T_C = create + instantiate + upload (Eq. 2) */
+  double exec_s;        /* T_E host wall: first launch call .. stream synchronized (Eq. 3) */
+  double gpu_s;         /* T_E on the device (CUDA events) */
+  int64_t kernels;      /* kernels executed by the call */
+  int64_t launches;     /* host launch API calls issued (kernel or graph launches) */
+  int64_t nodes;        /* nodes in the built graph (build only) */
+  int64_t graph_bytes;  /* device memory attributed to the instantiated+uploaded graph(s) */
+} ib_times;
+
+typedef struct ib_ctx ib_ctx;
+
+/* ---- library / device --------------------------------------------------------------------- */
+int ib_abi_version(void);
+const char *ib_last_error(void);
+int ib_device_count(int *count);
+/* HBM bytes free/total on a device (used for the paper's memory model m_base/m_node). */
+int ib_mem_info(int device, int64_t *free_bytes, int64_t *total_bytes);
+
+/* ---- context -------------------------------------------------------------------------------
+ * dims:    vector (N) ; hotspot2d (R, C) ; hotspot3d (R, C, L) ; fdtd (nx, ny, nz) cells.
+ * scalars: vector  [c]              (VectorWorkload.scale_constant, workloads.py:77)
+ *          hotspot [k]              (HotspotWorkload.diffusion_coefficient, workloads.py:120)
+ *          fdtd    [d, c_h, c_e]    (cell_size; dt/mu0; dt/eps0 — workloads.py:327-328,364-365)
+ *          Constants are passed in binary64 and rounded ONCE to the state dtype on the host,
+ *          except the vector constant in IB_F32 which stays binary64 (v' = (float)((double)v*c)).
+ * devices: one entry per slab; hotspot solvers partition axis 0 into ndevices slabs with the
+ *          reference's bounds formula rows*g//P (workloads.py:65). Device ids may repeat (several
+ *          slabs on one GPU: the halo exchange then goes through local memory, same graph).
+ *          vector / fdtd require ndevices == 1. NULL/0 means {current device}.
+ */
+int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
+              const double *scalars, int nscalars, const int *devices, int ndevices);
+void ib_destroy(ib_ctx *ctx);
+
+/* Fields, in the reference's state_arrays() order (workloads.py:93,163,272):
+ * vector: 0 values ; hotspot: 0 temperature, 1 power ; fdtd: 0 ex 1 ey 2 ez 3 hx 4 hy 5 hz.
+ * Host buffers are C-contiguous in the context dtype; bytes must equal the full field size. */
+int ib_num_fields(const ib_ctx *ctx);
+int ib_field_shape(const ib_ctx *ctx, int field, int64_t *shape3, int *ndim);
+int64_t ib_field_bytes(const ib_ctx *ctx, int field);
+int ib_upload(ib_ctx *ctx, int field, const void *host, size_t bytes);
+int ib_download(ib_ctx *ctx, int field, void *host, size_t bytes);
+/* Bytes one iteration moves by the roofline convention (every array read once, written once). */
+int64_t ib_iteration_bytes(const ib_ctx *ctx);
+
+/* ---- stream mode: run_loop (Listing 1) ------------------------------------------------------- */
+int ib_run_stream(ib_ctx *ctx, int64_t iterations, int flags, ib_times *times);
+/* One step of the chain program, for the per-step API (vector_scale_step, hotspot_step,
+ * fdtd_h_step = step 0, fdtd_e_step = step 1; workloads.py:97,167,325,358). */
+int ib_run_step(ib_ctx *ctx, int step, ib_times *times);
+int ib_num_steps(const ib_ctx *ctx);
+
+/* ---- graph mode: run_batched (Listings 2/3) -------------------------------------------------
+ * ib_graph_build unrolls batch_size iterations into one graph (2 nodes / iteration for fdtd;
+ * P nodes / iteration for P slabs), instantiates and uploads it on the context's non-blocking
+ * stream. Ping-pong parity: an even batch_size returns the buffers to their start parity, so one
+ * executable is replayed; an odd batch_size gets a second executable with swapped buffers and the
+ * two alternate (both are built and counted in T_C).
+ * ib_graph_run launches the executable num_batches times (or once, with IB_FLAG_WHILE). */
+int ib_graph_build(ib_ctx *ctx, int64_t batch_size, int build_mode, int flags, ib_times *times);
+int ib_graph_run(ib_ctx *ctx, int64_t num_batches, ib_times *times);
+int ib_graph_destroy(ib_ctx *ctx);
+int64_t ib_graph_batch_size(const ib_ctx *ctx);
+
+/* Device synchronisation of the context's streams. */
+int ib_sync(ib_ctx *ctx);
+
+/* ---- pinned host staging (used by the e2e path) -------------------------------------------- */
+int ib_host_alloc(void **ptr, size_t bytes);
+int ib_host_free(void *ptr);
+
+/* ---- checksum (workloads.py:508-525) ---------------------------------------------------------
+ * 64-bit FNV-1a, offset 0xcbf29ce484222325, prime 0x100000001b3, continued from h.
+ * ib_fnv1a64_f64 hashes the little-endian binary64 bytes of n values given in the context dtype
+ * (float values are widened exactly to binary64 first, as np.ascontiguousarray(a, "<f8") does). */
+uint64_t ib_fnv1a64(const void *data, size_t nbytes, uint64_t h);
+uint64_t ib_fnv1a64_f64(const void *values, size_t n, int dtype, uint64_t h);
+
+/* ---- L2 flush helper for benchmark hygiene (writes a buffer larger than L2) ----------------- */
+int ib_flush_l2(ib_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ITERBATCH_B200_H */

@@ -1,0 +1,214 @@
+"""Command line front end: ``python -m paper_2501_09398_b200 <command>``.
+
+``run-workload`` mirrors the reference's subcommand (pkg/src/iterbatch/cli.py:97-115,172-230):
+same flags, same seeded inputs (seed 20240817, cli.py:42,172-199), same checksum line and
+measurement CSV, executed on the B200 runtime. Extra flags: --dtype, --build, --pdl, --devices.
+
+``sweep`` runs the batch-size sweep the paper's model is fitted on: for every
+feasible K it records creation (T_C), graph execution (T_E) and stream execution, and writes one
+measurement CSV per kind in the reference schema, readable by ``iterbatch fit`` / ``speedup``.
+
+Exit codes as the reference (cli.py:3-4,253-263): 0 ok, 1 data errors (ValueError/OSError),
+2 usage errors.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+
+from .fitting import MeasurementPoint, MeasurementSeries, write_measurements_csv
+from .model import BatchPlan, feasible_batch_sizes
+
+WORKLOAD_SEED = 20240817  # cli.py:42
+
+
+class UsageError(Exception):
+    pass
+
+
+def _comma_sizes(text: str) -> list[int]:
+    try:
+        sizes = [int(part) for part in text.split(",")]
+    except ValueError:
+        raise argparse.ArgumentTypeError(f"sizes must be integers, got {text!r}")
+    if not sizes or any(s < 1 for s in sizes):
+        raise argparse.ArgumentTypeError(f"sizes must be positive, got {text!r}")
+    return sizes
+
+
+def build_workload(family: str, sizes: list[int]):
+    """The reference's synthetic inputs, value for value (cli.py:172-199)."""
+    from . import workloads as wl
+
+    rng = np.random.default_rng(WORKLOAD_SEED)
+    if family == "vector":
+        if len(sizes) != 1:
+            raise UsageError("vector takes one size: N")
+        return wl.VectorWorkload(rng.random(sizes[0]), 0.9999)
+    if family == "hotspot2d":
+        if len(sizes) not in (1, 2):
+            raise UsageError("hotspot2d takes N or N,N2 (rows, cols)")
+        shape = (sizes[0], sizes[-1])
+        return wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
+    if family == "hotspot3d":
+        if len(sizes) == 1:
+            shape = (sizes[0],) * 3
+        elif len(sizes) == 2:  # grid edge plus layer count
+            shape = (sizes[0], sizes[0], sizes[1])
+        elif len(sizes) == 3:
+            shape = tuple(sizes)
+        else:
+            raise UsageError("hotspot3d takes N, N,LAYERS, or N,N2,N3")
+        return wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
+    if family != "fdtd":
+        raise UsageError(f"unknown workload {family!r}")
+    if len(sizes) == 1:
+        nx = ny = nz = sizes[0]
+    elif len(sizes) == 3:
+        nx, ny, nz = sizes
+    else:
+        raise UsageError("fdtd takes N or N,N2,N3 (cells per axis)")
+    return wl.te101_cavity(nx, ny, nz)
+
+
+def programs():
+    from . import workloads as wl
+
+    return {
+        "vector": wl.vector_program,
+        "hotspot2d": wl.hotspot_program,
+        "hotspot3d": wl.hotspot_program,
+        "fdtd": wl.fdtd_program,
+    }
+
+
+def build_parser() -> argparse.ArgumentParser:
+    parser = argparse.ArgumentParser(
+        prog="iterbatch-b200",
+        description="Iteration-batched CUDA-graph execution of solver kernels on B200.",
+    )
+    commands = parser.add_subparsers(dest="command", required=True)
+
+    def common(p):
+        p.add_argument("--workload", choices=["vector", "hotspot2d", "hotspot3d", "fdtd"], required=True)
+        p.add_argument("--size", type=_comma_sizes, required=True, metavar="N[,N2[,N3]]")
+        p.add_argument("--iterations", type=int, required=True, metavar="I_K")
+        p.add_argument("--dtype", choices=["f64", "f32"], default="f64")
+        p.add_argument("--build", choices=["manual", "capture"], default="manual")
+        p.add_argument("--pdl", action="store_true", help="programmatic dependent launch edges")
+        p.add_argument("--devices", type=_comma_sizes, default=None,
+                       help="device id per axis-0 slab (hotspot only), e.g. 0,0 or 0,1,2,3")
+
+    run = commands.add_parser("run-workload", help="execute a workload and measure or checksum it")
+    common(run)
+    run.add_argument("--batch-size", type=int, required=True, metavar="S")
+    run.add_argument("--mode", choices=["loop", "batched"], required=True)
+    run.add_argument("--repeats", type=int, default=10)
+    run.add_argument("--timings", metavar="OUT.csv", help="write measured seconds")
+    run.add_argument("--checksum", action="store_true", help="print the final-state checksum")
+    run.set_defaults(func=_cmd_run_workload)
+
+    sw = commands.add_parser("sweep", help="measure T_C / T_E / stream time over batch sizes")
+    common(sw)
+    sw.add_argument("--batch-sizes", default="all",
+                    help="comma list, or 'all' for every divisor <= --max-fraction * I_K")
+    sw.add_argument("--max-fraction", type=float, default=0.25)
+    sw.add_argument("--repeats", type=int, default=10)
+    sw.add_argument("--out", required=True, metavar="DIR")
+    sw.set_defaults(func=_cmd_sweep)
+    return parser
+
+
+def _cmd_run_workload(args) -> int:
+    from . import workloads as wl
+
+    if not args.checksum and not args.timings:
+        raise UsageError("nothing to do: pass --checksum and/or --timings")
+    state = build_workload(args.workload, args.size)
+    program = programs()[args.workload]()
+    plan = BatchPlan.from_batch_size(args.iterations, args.batch_size)
+    order = wl.ExecutionOrder(args.mode)
+    kw = dict(dtype=args.dtype, devices=args.devices)
+    if args.checksum:
+        if order is wl.ExecutionOrder.LOOP:
+            final = wl.run_loop(program, state, plan.total_kernel_executions, pdl=args.pdl, **kw)
+        else:
+            final = wl.run_batched(program, state, plan.batch_size, plan.num_batches,
+                                   build=args.build, pdl=args.pdl, **kw)
+        print(f"{wl.state_checksum(final):016x}")
+    if args.timings:
+        series = wl.time_workload(program, state, plan, order, repeats=args.repeats,
+                                  label=args.workload, build=args.build, pdl=args.pdl, **kw)
+        write_measurements_csv(series, args.timings)
+    return 0
+
+
+def _cmd_sweep(args) -> int:
+    from . import workloads as wl
+
+    state = build_workload(args.workload, args.size)
+    program = programs()[args.workload]()
+    total = args.iterations
+    if args.batch_sizes == "all":
+        sizes = [k for k in feasible_batch_sizes(total) if k <= args.max_fraction * total]
+    else:
+        sizes = _comma_sizes(args.batch_sizes)
+    os.makedirs(args.out, exist_ok=True)
+    kw = dict(dtype=args.dtype, devices=args.devices, build=args.build, pdl=args.pdl)
+    creation, execution, stream, summary = [], [], [], []
+    for k in sizes:
+        plan = BatchPlan.from_batch_size(total, k)
+        g = wl.time_workload_phases(program, state, plan, wl.ExecutionOrder.BATCHED,
+                                    args.repeats, **kw)
+        s = wl.time_workload_phases(program, state, plan, wl.ExecutionOrder.LOOP,
+                                    args.repeats, **kw)
+        creation.append(MeasurementPoint(k, tuple(g["creation"])))
+        execution.append(MeasurementPoint(k, tuple(g["execution"])))
+        stream.append(MeasurementPoint(k, tuple(s["execution"])))
+        row = {
+            "batch_size": k,
+            "creation_s": statistics.fmean(g["creation"]),
+            "graph_exec_s": statistics.fmean(g["execution"]),
+            "graph_gpu_s": statistics.fmean(g["gpu"]),
+            "stream_exec_s": statistics.fmean(s["execution"]),
+            "stream_gpu_s": statistics.fmean(s["gpu"]),
+            "graph_bytes": g["times"][0][0].graph_bytes,
+            "nodes": g["times"][0][0].nodes,
+        }
+        row["us_per_iter_graph"] = 1e6 * row["graph_exec_s"] / total
+        row["us_per_iter_stream"] = 1e6 * row["stream_exec_s"] / total
+        row["speedup_exec"] = row["stream_exec_s"] / row["graph_exec_s"]
+        row["speedup_total"] = row["stream_exec_s"] / (row["graph_exec_s"] + row["creation_s"])
+        summary.append(row)
+        print(json.dumps(row), flush=True)
+    label = args.workload
+    write_measurements_csv(MeasurementSeries(tuple(creation), label), os.path.join(args.out, "creation.csv"))
+    write_measurements_csv(MeasurementSeries(tuple(execution), label), os.path.join(args.out, "execution.csv"))
+    write_measurements_csv(MeasurementSeries(tuple(stream), label), os.path.join(args.out, "stream.csv"))
+    with open(os.path.join(args.out, "summary.json"), "w") as fh:
+        json.dump({"workload": args.workload, "size": args.size, "iterations": total,
+                   "dtype": args.dtype, "build": args.build, "pdl": args.pdl, "rows": summary}, fh, indent=1)
+    return 0
+
+
+def main(argv=None) -> int:
+    parser = build_parser()
+    args = parser.parse_args(argv)
+    try:
+        return args.func(args)
+    except UsageError as exc:
+        print(f"usage error: {exc}", file=sys.stderr)
+        return 2
+    except (ValueError, OSError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

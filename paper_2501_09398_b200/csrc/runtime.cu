@@ -1,0 +1,1005 @@
+// runtime.cu — C++ launch layer behind include/iterbatch_b200.h.
+//
+// Replaces the bodies of the reference drivers (pkg/src/iterbatch/workloads.py):
+//   run_loop     workloads.py:442-450  -> ib_run_stream : N (2N for FDTD) launches from a C++ loop,
+//                                                          i.e. Listing 1
+//   run_batched  workloads.py:453-471  -> ib_graph_build + ib_graph_run : K iterations unrolled
+//                                          into one CUDA graph, instantiated and uploaded once,
+//                                          replayed I = N/K times (Listing 3)
+//   time_workload workloads.py:479-505 -> ib_times: T_C (create/instantiate/upload) separated
+//                                          from T_E (first launch .. sync)
+//   _fill_slabs  workloads.py:60-69    -> axis-0 slab decomposition rows*g//P across devices,
+//                                          halo planes pushed by the stencil kernel itself
+// The state lives in HBM for the whole run; the boundary is crossed by ib_upload/ib_download.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/iterbatch_b200.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define IB_CUDA(call)                                                                           \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess) {                                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? IB_ENOMEM : IB_ECUDA,                       \
+                  std::string(#call) + ": " + cudaGetErrorName(e_) + ": " + cudaGetErrorString(e_)); \
+    }                                                                                           \
+  } while (0)
+
+#define IB_TRY(expr)       \
+  do {                     \
+    int rc_ = (expr);      \
+    if (rc_ != IB_OK) return rc_; \
+  } while (0)
+
+using clk = std::chrono::steady_clock;
+double secs(clk::time_point a, clk::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+// Restores the caller's current device (torch and other libraries rely on it).
+struct DeviceGuard {
+  int saved = -1;
+  DeviceGuard() { cudaGetDevice(&saved); }
+  ~DeviceGuard() {
+    if (saved >= 0) cudaSetDevice(saved);
+  }
+};
+
+// A kernel launch with its argument values stored by value (graph nodes copy them at add time).
+struct Launch {
+  const void *func = nullptr;
+  dim3 grid, block;
+  int slab = 0;
+  int nargs = 0;
+  alignas(16) unsigned char slot[16][16];
+  void *ptr[16];
+  void **args() {
+    for (int i = 0; i < nargs; ++i) ptr[i] = slot[i];
+    return ptr;
+  }
+};
+
+template <typename A>
+void put_args(Launch &L, A a) {
+  static_assert(sizeof(A) <= 16, "kernel argument too large");
+  std::memcpy(L.slot[L.nargs++], &a, sizeof(A));
+}
+template <typename A, typename... R>
+void put_args(Launch &L, A a, R... rest) {
+  put_args(L, a);
+  put_args(L, rest...);
+}
+template <typename... Args>
+Launch make_launch(const void *func, dim3 grid, dim3 block, int slab, Args... args) {
+  Launch L;
+  L.func = func;
+  L.grid = grid;
+  L.block = block;
+  L.slab = slab;
+  put_args(L, args...);
+  return L;
+}
+
+struct Slab {
+  int device = 0;
+  int row_lo = 0, row_hi = 0;  // global rows owned [lo, hi)
+  bool has_top = false, has_bot = false;
+  void *buf[2] = {nullptr, nullptr};  // (rows_local + 2) planes each: halo, owned..., halo
+  void *power = nullptr;              // rows_local planes
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};  // "iteration t done" double buffer for neighbours
+  cudaEvent_t join = nullptr;              // fork/join of the slab streams
+  int rows() const { return row_hi - row_lo; }
+};
+
+int64_t env_int(const char *name, int64_t dflt) {
+  const char *v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::strtoll(v, nullptr, 10);
+}
+
+}  // namespace
+
+struct ib_ctx {
+  int solver = 0, dtype = 0, esize = 8;
+  int64_t dims[3] = {1, 1, 1};
+  int ndims = 1;
+  double scalars[3] = {0, 0, 0};
+  std::vector<Slab> slabs;
+  void *field[6] = {};      // vector / fdtd device fields (single slab)
+  int64_t fshape[6][3] = {};
+  int fndim[6] = {};
+  int nfields = 0;
+  int cur = 0;              // hotspot ping-pong parity: buf[cur] holds the current temperature
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaStream_t cap_stream = nullptr;  // used only for stream capture of single-slab graphs
+  // graph state
+  int64_t K = 0;
+  int gflags = 0, gmode = 0;
+  cudaGraph_t graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // indexed by start parity
+  cudaGraphConditionalHandle cond[2] = {};
+  int *d_counter = nullptr;  // WHILE-mode remaining-batch counter
+  void *flush = nullptr;
+  size_t flush_bytes = 0;
+
+  cudaStream_t stream() const { return slabs[0].stream; }
+  bool ping_pong() const {
+    return solver == IB_SOLVER_HOTSPOT2D || solver == IB_SOLVER_HOTSPOT3D;
+  }
+  int64_t plane() const {  // elements per axis-0 plane (hotspot)
+    return solver == IB_SOLVER_HOTSPOT3D ? dims[1] * dims[2] : dims[1];
+  }
+};
+
+namespace {
+
+int64_t numel(const int64_t *s, int n) {
+  int64_t r = 1;
+  for (int i = 0; i < n; ++i) r *= s[i];
+  return r;
+}
+
+// ---- per-iteration launch lists ----------------------------------------------------------------
+int hotspot_rows_per_chunk(const ib_ctx *c, int rows) {
+  int64_t rpc = env_int("IB_HOTSPOT_RPC", 0);
+  if (rpc <= 0) {
+    const int64_t want_threads = 148LL * 2048 * 2;
+    int64_t chunks = (want_threads + c->plane() - 1) / c->plane();
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, rows));
+    rpc = (rows + chunks - 1) / chunks;
+    rpc = std::min<int64_t>(rpc, 64);
+  }
+  return (int)std::max<int64_t>(1, std::min<int64_t>(rpc, rows));
+}
+
+template <typename T>
+void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
+  const int C = (int)c->dims[1];
+  const int L = d3 ? (int)c->dims[2] : 1;
+  const int64_t plane = c->plane();
+  const T k = (T)c->scalars[0];
+  const T loss = (T)(2.0 * (d3 ? 3 : 2));
+  const void *fn = d3 ? (const void *)ib::k_hotspot<T, true> : (const void *)ib::k_hotspot<T, false>;
+  const int P = (int)c->slabs.size();
+  const bool multi = P > 1;
+  for (int g = 0; g < P; ++g) {
+    Slab &s = c->slabs[g];
+    const int rows = s.rows();
+    const int rpc = hotspot_rows_per_chunk(c, rows);
+    const int64_t off = multi ? plane : 0;  // first owned plane
+    const T *src = (const T *)s.buf[parity] + off;
+    T *dst = (T *)s.buf[parity ^ 1] + off;
+    T *up = nullptr, *dn = nullptr;
+    if (multi && g > 0) {  // my first owned row -> upper neighbour's bottom halo
+      Slab &n = c->slabs[g - 1];
+      up = (T *)n.buf[parity ^ 1] + (int64_t)(n.rows() + 1) * plane;
+    }
+    if (multi && g + 1 < P) {  // my last owned row -> lower neighbour's top halo
+      Slab &n = c->slabs[g + 1];
+      dn = (T *)n.buf[parity ^ 1];
+    }
+    dim3 block(256);
+    dim3 grid((unsigned)((plane + 255) / 256), (unsigned)((rows + rpc - 1) / rpc));
+    out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, rpc, k,
+                              loss, (int)s.has_top, (int)s.has_bot, up, dn));
+  }
+}
+
+template <typename T>
+void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
+  const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
+  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
+  const int unit = (c->scalars[0] == 1.0) ? 1 : 0;
+  T **f = (T **)c->field;
+  const int64_t pl = (int64_t)(ny + 1) * (nz + 1);
+  dim3 block(256);
+  dim3 grid((unsigned)((pl + 255) / 256), (unsigned)(nx + 1));
+  out.push_back(make_launch((const void *)ib::k_fdtd_h<T>, grid, block, 0, (const T *)f[0],
+                            (const T *)f[1], (const T *)f[2], f[3], f[4], f[5], nx, ny, nz, ch, d,
+                            unit));
+  out.push_back(make_launch((const void *)ib::k_fdtd_e<T>, grid, block, 0, f[0], f[1], f[2],
+                            (const T *)f[3], (const T *)f[4], (const T *)f[5], nx, ny, nz, ce, d,
+                            unit));
+}
+
+void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  out.clear();
+  switch (c->solver) {
+    case IB_SOLVER_VECTOR: {
+      const int64_t n = c->dims[0];
+      const double cc = c->scalars[0];
+      if (c->dtype == IB_F32) {
+        const int64_t threads = (n >> 2) + (n & 3);
+        dim3 block(128), grid((unsigned)((threads + 127) / 128));
+        out.push_back(make_launch((const void *)ib::k_vector_f32, grid, block, 0,
+                                  (float *)c->field[0], n, cc));
+      } else {
+        const int64_t threads = (n >> 1) + (n & 1);
+        dim3 block(128), grid((unsigned)((threads + 127) / 128));
+        out.push_back(make_launch((const void *)ib::k_vector_f64, grid, block, 0,
+                                  (double *)c->field[0], n, cc));
+      }
+      break;
+    }
+    case IB_SOLVER_HOTSPOT2D:
+    case IB_SOLVER_HOTSPOT3D:
+      if (c->dtype == IB_F32)
+        hotspot_launches<float>(c, parity, out);
+      else
+        hotspot_launches<double>(c, parity, out);
+      break;
+    case IB_SOLVER_FDTD:
+      if (c->dtype == IB_F32)
+        fdtd_launches<float>(c, out);
+      else
+        fdtd_launches<double>(c, out);
+      break;
+  }
+}
+
+int launch_one(Launch &L, cudaStream_t s, bool pdl) {
+  if (!pdl) {
+    IB_CUDA(cudaLaunchKernel(L.func, L.grid, L.block, L.args(), 0, s));
+    return IB_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = L.grid;
+  cfg.blockDim = L.block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  IB_CUDA(cudaLaunchKernelExC(&cfg, L.func, L.args()));
+  return IB_OK;
+}
+
+// Enqueue `iters` iterations starting at `parity` onto the slab streams (also used under stream
+// capture). Multi-slab: kernel(g,t) waits for kernel(g+-1,t-1) — RAW on the halo it reads and
+// WAR on the halo it writes — through double-buffered events.
+int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStream_t single_stream,
+                       int64_t *kernels, int64_t *launches) {
+  std::vector<Launch> its[2];
+  iteration_launches(c, 0, its[0]);
+  if (c->ping_pong()) iteration_launches(c, 1, its[1]);
+  const int P = (int)c->slabs.size();
+  int par = parity;
+  int64_t nk = 0;
+  for (int64_t t = 0; t < iters; ++t) {
+    std::vector<Launch> &v = c->ping_pong() ? its[par] : its[0];
+    for (size_t q = 0; q < v.size(); ++q) {
+      Launch &L = v[q];
+      Slab &s = c->slabs[L.slab];
+      cudaStream_t st = (P == 1 && single_stream) ? single_stream : s.stream;
+      if (P > 1) {
+        IB_CUDA(cudaSetDevice(s.device));
+        if (t > 0) {
+          if (L.slab > 0) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab - 1].ev[(t - 1) & 1], 0));
+          if (L.slab + 1 < P) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab + 1].ev[(t - 1) & 1], 0));
+        }
+      }
+      // PDL only chains kernels on the same stream; the very first launch has no predecessor.
+      const bool use_pdl = pdl && P == 1 && (t > 0 || q > 0);
+      IB_TRY(launch_one(L, st, use_pdl));
+      if (P > 1) IB_CUDA(cudaEventRecord(s.ev[t & 1], st));
+      ++nk;
+    }
+    if (c->ping_pong()) par ^= 1;
+  }
+  if (P > 1) IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  if (kernels) *kernels += nk;
+  if (launches) *launches += nk;
+  return IB_OK;
+}
+
+// Join all slab streams into slab 0's stream (or fork from it).
+int join_into(ib_ctx *c, cudaStream_t root, bool fork) {
+  if (c->slabs.size() == 1) return IB_OK;
+  if (fork) {
+    IB_CUDA(cudaSetDevice(c->slabs[0].device));
+    IB_CUDA(cudaEventRecord(c->slabs[0].join, root));
+  }
+  for (size_t g = 1; g < c->slabs.size(); ++g) {
+    Slab &s = c->slabs[g];
+    IB_CUDA(cudaSetDevice(s.device));
+    if (fork) {
+      IB_CUDA(cudaStreamWaitEvent(s.stream, c->slabs[0].join, 0));
+    } else {
+      IB_CUDA(cudaEventRecord(s.join, s.stream));
+      IB_CUDA(cudaSetDevice(c->slabs[0].device));
+      IB_CUDA(cudaStreamWaitEvent(root, s.join, 0));
+    }
+  }
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  return IB_OK;
+}
+
+void free_graphs(ib_ctx *c) {
+  for (int p = 0; p < 2; ++p) {
+    if (c->exec[p]) cudaGraphExecDestroy(c->exec[p]);
+    if (c->graph[p]) cudaGraphDestroy(c->graph[p]);
+    c->exec[p] = nullptr;
+    c->graph[p] = nullptr;
+  }
+  c->K = 0;
+}
+
+// Listing 3: cudaGraphCreate + a linear chain of cudaGraphAddKernelNode.
+// With IB_FLAG_PDL the chain edges are programmatic (kernel t+1 may be resident before t ends).
+int build_manual_chain(ib_ctx *c, cudaGraph_t graph, int64_t K, int parity, bool pdl,
+                       cudaGraphNode_t *first, cudaGraphNode_t *last, int64_t *nodes) {
+  std::vector<Launch> its[2];
+  iteration_launches(c, 0, its[0]);
+  if (c->ping_pong()) iteration_launches(c, 1, its[1]);
+  cudaGraphNode_t prev = nullptr;
+  int par = parity;
+  for (int64_t t = 0; t < K; ++t) {
+    std::vector<Launch> &v = c->ping_pong() ? its[par] : its[0];
+    for (Launch &L : v) {
+      cudaKernelNodeParams np = {};
+      np.func = const_cast<void *>(L.func);
+      np.gridDim = L.grid;
+      np.blockDim = L.block;
+      np.sharedMemBytes = 0;
+      np.kernelParams = L.args();
+      np.extra = nullptr;
+      cudaGraphNode_t node;
+      if (!prev) {
+        IB_CUDA(cudaGraphAddKernelNode(&node, graph, nullptr, 0, &np));
+        if (first) *first = node;
+      } else if (!pdl) {
+        IB_CUDA(cudaGraphAddKernelNode(&node, graph, &prev, 1, &np));
+      } else {
+        IB_CUDA(cudaGraphAddKernelNode(&node, graph, nullptr, 0, &np));
+        cudaGraphEdgeData ed = {};
+        ed.from_port = cudaGraphKernelNodePortProgrammatic;
+        ed.type = cudaGraphDependencyTypeProgrammatic;
+        IB_CUDA(cudaGraphAddDependencies_v2(graph, &prev, &node, &ed, 1));
+      }
+      prev = node;
+      ++*nodes;
+    }
+    if (c->ping_pong()) par ^= 1;
+  }
+  if (last) *last = prev;
+  return IB_OK;
+}
+
+}  // namespace
+
+// Device-side tail of a WHILE body: decrement the remaining-batch counter and keep looping while
+// batches remain (cudaGraphSetConditional, CUDA 12.4+ conditional nodes).
+__global__ void k_while_tick(int *counter, cudaGraphConditionalHandle h) {
+  int left = *counter - 1;
+  *counter = left;
+  cudaGraphSetConditional(h, left > 0 ? 1u : 0u);
+}
+
+namespace {
+
+// Build one executable graph starting at `parity`.
+int build_one(ib_ctx *c, int parity, ib_times *tm) {
+  const bool pdl = (c->gflags & IB_FLAG_PDL) != 0;
+  const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
+  const int P = (int)c->slabs.size();
+  int64_t nodes = 0;
+  auto a = clk::now();
+  cudaGraph_t g = nullptr;
+  if (c->gmode == IB_BUILD_MANUAL && P == 1) {
+    IB_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraph_t body = g;
+    if (wh) {
+      // graph = [WHILE node { K-chain ; tick }]; the counter is set before each launch.
+      IB_CUDA(cudaGraphConditionalHandleCreate(&c->cond[parity], g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = c->cond[parity];
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t wnode;
+      IB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &cp));
+      body = cp.conditional.phGraph_out[0];
+      ++nodes;
+    }
+    cudaGraphNode_t last = nullptr;
+    IB_TRY(build_manual_chain(c, body, c->K, parity, pdl, nullptr, &last, &nodes));
+    if (wh) {
+      cudaKernelNodeParams np = {};
+      int *cnt = c->d_counter;
+      cudaGraphConditionalHandle h = c->cond[parity];
+      void *args[2] = {&cnt, &h};
+      np.func = (void *)k_while_tick;
+      np.gridDim = dim3(1);
+      np.blockDim = dim3(1);
+      np.kernelParams = args;
+      cudaGraphNode_t tick;
+      IB_CUDA(cudaGraphAddKernelNode(&tick, body, &last, 1, &np));
+      ++nodes;
+    }
+  } else {
+    if (wh) return fail(IB_EINVAL, "IB_FLAG_WHILE requires IB_BUILD_MANUAL on a single slab");
+    // Stream capture of exactly the stream-mode launch sequence.
+    cudaStream_t root = (P == 1) ? c->cap_stream : c->slabs[0].stream;
+    IB_CUDA(cudaSetDevice(c->slabs[0].device));
+    IB_CUDA(cudaStreamBeginCapture(root, cudaStreamCaptureModeThreadLocal));
+    int rc = join_into(c, root, true);
+    int64_t kk = 0, ll = 0;
+    if (rc == IB_OK) rc = enqueue_iterations(c, c->K, parity, pdl, P == 1 ? root : nullptr, &kk, &ll);
+    if (rc == IB_OK) rc = join_into(c, root, false);
+    cudaError_t e = cudaStreamEndCapture(root, &g);
+    if (rc != IB_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    IB_CUDA(e);
+    size_t n = 0;
+    IB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    nodes += (int64_t)n;
+  }
+  auto b = clk::now();
+  unsigned long long iflags = 0;
+  if (c->gflags & IB_FLAG_DEVICE_LAUNCH) iflags |= cudaGraphInstantiateFlagDeviceLaunch;
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t ie = cudaGraphInstantiateWithFlags(&ex, g, iflags);
+  if (ie != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return fail(IB_ECUDA, std::string("cudaGraphInstantiateWithFlags: ") + cudaGetErrorString(ie));
+  }
+  auto d = clk::now();
+  if (!(c->gflags & IB_FLAG_NO_UPLOAD)) {
+    IB_CUDA(cudaGraphUpload(ex, c->stream()));
+    IB_CUDA(cudaStreamSynchronize(c->stream()));
+  }
+  auto e2 = clk::now();
+  c->graph[parity] = g;
+  c->exec[parity] = ex;
+  if (tm) {
+    tm->create_s += secs(a, b);
+    tm->instantiate_s += secs(b, d);
+    tm->upload_s += secs(d, e2);
+    tm->build_s += secs(a, e2);
+    tm->nodes += nodes;
+  }
+  return IB_OK;
+}
+
+int check_ctx(const ib_ctx *c) {
+  if (!c) return fail(IB_EINVAL, "null context");
+  return IB_OK;
+}
+
+}  // namespace
+
+// ================================================================================================
+// C ABI
+// ================================================================================================
+extern "C" {
+
+int ib_abi_version(void) { return IB_ABI_VERSION; }
+
+const char *ib_last_error(void) { return g_err.c_str(); }
+
+int ib_device_count(int *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) n = 0;
+  if (count) *count = n;
+  if (n == 0) return fail(IB_ENODEV, "no CUDA device visible");
+  return IB_OK;
+}
+
+int ib_mem_info(int device, int64_t *free_bytes, int64_t *total_bytes) {
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(device));
+  size_t f = 0, t = 0;
+  IB_CUDA(cudaMemGetInfo(&f, &t));
+  if (free_bytes) *free_bytes = (int64_t)f;
+  if (total_bytes) *total_bytes = (int64_t)t;
+  return IB_OK;
+}
+
+void ib_destroy(ib_ctx *c) {
+  if (!c) return;
+  DeviceGuard guard;
+  if (!c->slabs.empty()) cudaSetDevice(c->slabs[0].device);
+  free_graphs(c);
+  for (Slab &s : c->slabs) {
+    cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    for (int p = 0; p < 2; ++p) {
+      if (s.buf[p]) cudaFree(s.buf[p]);
+      if (s.ev[p]) cudaEventDestroy(s.ev[p]);
+    }
+    if (s.power) cudaFree(s.power);
+    if (s.join) cudaEventDestroy(s.join);
+    if (s.stream) cudaStreamDestroy(s.stream);
+  }
+  if (!c->slabs.empty()) cudaSetDevice(c->slabs[0].device);
+  for (int f = 0; f < 6; ++f)
+    if (c->field[f]) cudaFree(c->field[f]);
+  if (c->d_counter) cudaFree(c->d_counter);
+  if (c->flush) cudaFree(c->flush);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  delete c;
+}
+
+static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
+  const int P = ndevices;
+  const bool hot = c->ping_pong();
+  if (P > 1 && !hot) return fail(IB_EINVAL, "multi-slab execution is only defined for hotspot solvers");
+  const int64_t rows = hot ? c->dims[0] : 1;
+  if (P > rows) return fail(IB_EINVAL, "more slabs than rows along axis 0");
+  c->slabs.resize(P);
+  for (int g = 0; g < P; ++g) {
+    Slab &s = c->slabs[g];
+    s.device = devices[g];
+    s.row_lo = (int)(rows * g / P);  // workloads.py:65 bounds formula
+    s.row_hi = (int)(rows * (g + 1) / P);
+    s.has_top = g > 0;
+    s.has_bot = g + 1 < P;
+    IB_CUDA(cudaSetDevice(s.device));
+    IB_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    for (int p = 0; p < 2; ++p) IB_CUDA(cudaEventCreateWithFlags(&s.ev[p], cudaEventDisableTiming));
+    IB_CUDA(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming));
+  }
+  // peer access between neighbouring slabs on different devices (NVLink P2P stores)
+  for (int g = 0; g + 1 < P; ++g) {
+    int a = c->slabs[g].device, b = c->slabs[g + 1].device;
+    if (a == b) continue;
+    int ok = 0;
+    IB_CUDA(cudaDeviceCanAccessPeer(&ok, a, b));
+    if (!ok) return fail(IB_EINVAL, "devices " + std::to_string(a) + "," + std::to_string(b) + " lack peer access");
+    for (int dir = 0; dir < 2; ++dir) {
+      IB_CUDA(cudaSetDevice(dir ? b : a));
+      cudaError_t e = cudaDeviceEnablePeerAccess(dir ? a : b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else IB_CUDA(e);
+    }
+  }
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_CUDA(cudaEventCreate(&c->t0));
+  IB_CUDA(cudaEventCreate(&c->t1));
+  IB_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  IB_CUDA(cudaMalloc(&c->d_counter, sizeof(int)));
+  const int es = c->esize;
+  if (hot) {
+    const int64_t plane = c->plane();
+    for (Slab &s : c->slabs) {
+      IB_CUDA(cudaSetDevice(s.device));
+      const int64_t planes = s.rows() + (P > 1 ? 2 : 0);
+      for (int p = 0; p < 2; ++p) {
+        IB_CUDA(cudaMalloc(&s.buf[p], (size_t)(planes * plane * es)));
+        IB_CUDA(cudaMemset(s.buf[p], 0, (size_t)(planes * plane * es)));
+      }
+      IB_CUDA(cudaMalloc(&s.power, (size_t)(s.rows() * plane * es)));
+      IB_CUDA(cudaMemset(s.power, 0, (size_t)(s.rows() * plane * es)));
+    }
+    IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  } else {
+    for (int f = 0; f < c->nfields; ++f) {
+      const size_t b = (size_t)(numel(c->fshape[f], c->fndim[f]) * es);
+      IB_CUDA(cudaMalloc(&c->field[f], b));
+      IB_CUDA(cudaMemset(c->field[f], 0, b));
+    }
+  }
+  IB_CUDA(cudaDeviceSynchronize());
+  return IB_OK;
+}
+
+int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
+              const double *scalars, int nscalars, const int *devices, int ndevices) {
+  if (!out) return fail(IB_EINVAL, "out is null");
+  *out = nullptr;
+  if (solver < IB_SOLVER_VECTOR || solver > IB_SOLVER_FDTD) return fail(IB_EINVAL, "unknown solver");
+  if (dtype != IB_F32 && dtype != IB_F64) return fail(IB_EINVAL, "dtype must be IB_F32 or IB_F64");
+  static const int want_nd[4] = {1, 2, 3, 3};
+  static const int want_ns[4] = {1, 1, 1, 3};
+  if (ndims != want_nd[solver] || !dims)
+    return fail(IB_EINVAL, "solver expects " + std::to_string(want_nd[solver]) + " dims, got " + std::to_string(ndims));
+  if (nscalars != want_ns[solver] || !scalars)
+    return fail(IB_EINVAL, "solver expects " + std::to_string(want_ns[solver]) + " scalars");
+  for (int i = 0; i < ndims; ++i)
+    if (dims[i] < 1) return fail(IB_EINVAL, "dims must be >= 1");
+  if (solver != IB_SOLVER_VECTOR) {
+    for (int i = 0; i < ndims; ++i)
+      if (dims[i] > (1LL << 30)) return fail(IB_EINVAL, "dimension too large");
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(IB_ENODEV, "no CUDA device visible (this library has no CPU fallback)");
+  }
+  std::vector<int> devs;
+  if (!devices || ndevices <= 0) {
+    int d = 0;
+    IB_CUDA(cudaGetDevice(&d));
+    devs.push_back(d);
+  } else {
+    for (int i = 0; i < ndevices; ++i) {
+      if (devices[i] < 0 || devices[i] >= ndev) return fail(IB_EINVAL, "device id out of range");
+      devs.push_back(devices[i]);
+    }
+  }
+  DeviceGuard guard;
+  ib_ctx *c = new ib_ctx();
+  c->solver = solver;
+  c->dtype = dtype;
+  c->esize = dtype == IB_F32 ? 4 : 8;
+  c->ndims = ndims;
+  for (int i = 0; i < ndims; ++i) c->dims[i] = dims[i];
+  for (int i = 0; i < nscalars; ++i) c->scalars[i] = scalars[i];
+  if (solver == IB_SOLVER_FDTD && !(scalars[0] > 0.0)) {
+    delete c;
+    return fail(IB_EINVAL, "cell_size must be positive");
+  }
+  if (solver == IB_SOLVER_VECTOR) {
+    c->nfields = 1;
+    c->fndim[0] = 1;
+    c->fshape[0][0] = dims[0];
+  } else if (solver == IB_SOLVER_FDTD) {
+    const int64_t nx = dims[0], ny = dims[1], nz = dims[2];
+    const int64_t sh[6][3] = {{nx, ny + 1, nz + 1}, {nx + 1, ny, nz + 1}, {nx + 1, ny + 1, nz},
+                              {nx + 1, ny, nz},     {nx, ny + 1, nz},     {nx, ny, nz + 1}};
+    c->nfields = 6;
+    for (int f = 0; f < 6; ++f) {
+      c->fndim[f] = 3;
+      for (int a = 0; a < 3; ++a) c->fshape[f][a] = sh[f][a];
+    }
+    if ((nx + 1) > 65535) {
+      delete c;
+      return fail(IB_EINVAL, "fdtd nx must be < 65535");
+    }
+  } else {
+    c->nfields = 2;
+    for (int f = 0; f < 2; ++f) {
+      c->fndim[f] = ndims;
+      for (int a = 0; a < ndims; ++a) c->fshape[f][a] = dims[a];
+    }
+  }
+  int rc = create_impl(c, devs.data(), (int)devs.size());
+  if (rc != IB_OK) {
+    std::string msg = g_err;
+    ib_destroy(c);
+    g_err = msg;
+    return rc;
+  }
+  *out = c;
+  return IB_OK;
+}
+
+int ib_num_fields(const ib_ctx *c) { return c ? c->nfields : 0; }
+
+int ib_field_shape(const ib_ctx *c, int field, int64_t *shape3, int *ndim) {
+  IB_TRY(check_ctx(c));
+  if (field < 0 || field >= c->nfields) return fail(IB_EINVAL, "field index out of range");
+  if (ndim) *ndim = c->fndim[field];
+  if (shape3)
+    for (int a = 0; a < 3; ++a) shape3[a] = a < c->fndim[field] ? c->fshape[field][a] : 1;
+  return IB_OK;
+}
+
+int64_t ib_field_bytes(const ib_ctx *c, int field) {
+  if (!c || field < 0 || field >= c->nfields) return -1;
+  return numel(c->fshape[field], c->fndim[field]) * c->esize;
+}
+
+int64_t ib_iteration_bytes(const ib_ctx *c) {
+  if (!c) return -1;
+  const int64_t es = c->esize;
+  switch (c->solver) {
+    case IB_SOLVER_VECTOR: return 2 * c->dims[0] * es;
+    case IB_SOLVER_HOTSPOT2D:
+    case IB_SOLVER_HOTSPOT3D: return 3 * numel(c->dims, c->ndims) * es;
+    case IB_SOLVER_FDTD: {
+      int64_t e = 0, h = 0;
+      for (int f = 0; f < 3; ++f) e += numel(c->fshape[f], 3);
+      for (int f = 3; f < 6; ++f) h += numel(c->fshape[f], 3);
+      return (e + 2 * h + h + 2 * e) * es;  // H half-step + E half-step
+    }
+  }
+  return -1;
+}
+
+static int hotspot_copy(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
+  const int64_t plane = c->plane();
+  const int64_t pb = plane * c->esize;
+  const int P = (int)c->slabs.size();
+  char *h = (char *)host;
+  for (int g = 0; g < P; ++g) {
+    Slab &s = c->slabs[g];
+    IB_CUDA(cudaSetDevice(s.device));
+    const int64_t off = (P > 1) ? pb : 0;
+    char *dev = field == 0 ? (char *)s.buf[c->cur] + off : (char *)s.power;
+    const size_t nb = (size_t)(s.rows() * pb);
+    if (up) {
+      IB_CUDA(cudaMemcpyAsync(dev, h + s.row_lo * pb, nb, cudaMemcpyHostToDevice, s.stream));
+      if (field == 0 && s.has_top)
+        IB_CUDA(cudaMemcpyAsync((char *)s.buf[c->cur], h + (s.row_lo - 1) * pb, (size_t)pb,
+                                cudaMemcpyHostToDevice, s.stream));
+      if (field == 0 && s.has_bot)
+        IB_CUDA(cudaMemcpyAsync((char *)s.buf[c->cur] + (int64_t)(s.rows() + 1) * pb,
+                                h + (int64_t)s.row_hi * pb, (size_t)pb, cudaMemcpyHostToDevice, s.stream));
+    } else {
+      IB_CUDA(cudaMemcpyAsync(h + s.row_lo * pb, dev, nb, cudaMemcpyDeviceToHost, s.stream));
+    }
+  }
+  (void)bytes;
+  for (Slab &s : c->slabs) {
+    IB_CUDA(cudaSetDevice(s.device));
+    IB_CUDA(cudaStreamSynchronize(s.stream));
+  }
+  return IB_OK;
+}
+
+static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
+  IB_TRY(check_ctx(c));
+  if (field < 0 || field >= c->nfields) return fail(IB_EINVAL, "field index out of range");
+  if (!host) return fail(IB_EINVAL, "host pointer is null");
+  const int64_t want = ib_field_bytes(c, field);
+  if ((int64_t)bytes != want)
+    return fail(IB_EINVAL, "field " + std::to_string(field) + " holds " + std::to_string(want) +
+                               " bytes, got " + std::to_string(bytes));
+  DeviceGuard guard;
+  if (c->ping_pong()) return hotspot_copy(c, field, host, bytes, up);
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  if (up)
+    IB_CUDA(cudaMemcpyAsync(c->field[field], host, bytes, cudaMemcpyHostToDevice, c->stream()));
+  else
+    IB_CUDA(cudaMemcpyAsync(host, c->field[field], bytes, cudaMemcpyDeviceToHost, c->stream()));
+  IB_CUDA(cudaStreamSynchronize(c->stream()));
+  return IB_OK;
+}
+
+int ib_upload(ib_ctx *c, int field, const void *host, size_t bytes) {
+  return xfer(c, field, const_cast<void *>(host), bytes, true);
+}
+int ib_download(ib_ctx *c, int field, void *host, size_t bytes) {
+  return xfer(c, field, host, bytes, false);
+}
+
+int ib_sync(ib_ctx *c) {
+  IB_TRY(check_ctx(c));
+  DeviceGuard guard;
+  for (Slab &s : c->slabs) {
+    IB_CUDA(cudaSetDevice(s.device));
+    IB_CUDA(cudaStreamSynchronize(s.stream));
+  }
+  return IB_OK;
+}
+
+static int sync_all(ib_ctx *c) {
+  for (Slab &s : c->slabs) {
+    IB_CUDA(cudaSetDevice(s.device));
+    IB_CUDA(cudaStreamSynchronize(s.stream));
+  }
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  return IB_OK;
+}
+
+int ib_run_stream(ib_ctx *c, int64_t iterations, int flags, ib_times *tm) {
+  IB_TRY(check_ctx(c));
+  if (iterations < 0) return fail(IB_EINVAL, "total_iterations must be >= 0");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_TRY(sync_all(c));
+  ib_times t = {};
+  const bool pdl = (flags & IB_FLAG_PDL) != 0;
+  auto a = clk::now();
+  IB_CUDA(cudaEventRecord(c->t0, c->stream()));
+  IB_TRY(join_into(c, c->stream(), true));
+  IB_TRY(enqueue_iterations(c, iterations, c->cur, pdl, nullptr, &t.kernels, &t.launches));
+  IB_TRY(join_into(c, c->stream(), false));
+  IB_CUDA(cudaEventRecord(c->t1, c->stream()));
+  IB_CUDA(cudaEventSynchronize(c->t1));
+  IB_TRY(sync_all(c));
+  auto b = clk::now();
+  float ms = 0;
+  IB_CUDA(cudaEventElapsedTime(&ms, c->t0, c->t1));
+  if (c->ping_pong() && (iterations & 1)) c->cur ^= 1;
+  t.exec_s = secs(a, b);
+  t.gpu_s = ms * 1e-3;
+  if (tm) *tm = t;
+  return IB_OK;
+}
+
+int ib_num_steps(const ib_ctx *c) { return c ? (c->solver == IB_SOLVER_FDTD ? 2 : 1) : 0; }
+
+int ib_run_step(ib_ctx *c, int step, ib_times *tm) {
+  IB_TRY(check_ctx(c));
+  if (step < 0 || step >= ib_num_steps(c)) return fail(IB_EINVAL, "step index out of range");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_TRY(sync_all(c));
+  std::vector<Launch> v;
+  iteration_launches(c, c->cur, v);
+  ib_times t = {};
+  auto a = clk::now();
+  IB_CUDA(cudaEventRecord(c->t0, c->stream()));
+  IB_TRY(join_into(c, c->stream(), true));
+  for (Launch &L : v) {
+    if (c->solver == IB_SOLVER_FDTD && &L != &v[step]) continue;
+    Slab &s = c->slabs[L.slab];
+    IB_CUDA(cudaSetDevice(s.device));
+    IB_TRY(launch_one(L, s.stream, false));
+    ++t.kernels;
+  }
+  IB_TRY(join_into(c, c->stream(), false));
+  IB_CUDA(cudaEventRecord(c->t1, c->stream()));
+  IB_CUDA(cudaEventSynchronize(c->t1));
+  IB_TRY(sync_all(c));
+  auto b = clk::now();
+  float ms = 0;
+  IB_CUDA(cudaEventElapsedTime(&ms, c->t0, c->t1));
+  if (c->ping_pong()) c->cur ^= 1;
+  t.launches = t.kernels;
+  t.exec_s = secs(a, b);
+  t.gpu_s = ms * 1e-3;
+  if (tm) *tm = t;
+  return IB_OK;
+}
+
+int ib_graph_destroy(ib_ctx *c) {
+  IB_TRY(check_ctx(c));
+  DeviceGuard guard;
+  cudaSetDevice(c->slabs[0].device);
+  free_graphs(c);
+  return IB_OK;
+}
+
+int64_t ib_graph_batch_size(const ib_ctx *c) { return c ? c->K : -1; }
+
+int ib_graph_build(ib_ctx *c, int64_t batch_size, int build_mode, int flags, ib_times *tm) {
+  IB_TRY(check_ctx(c));
+  if (batch_size < 1) return fail(IB_EINVAL, "batch_size must be >= 1");
+  if (build_mode != IB_BUILD_MANUAL && build_mode != IB_BUILD_CAPTURE)
+    return fail(IB_EINVAL, "unknown build mode");
+  if ((flags & IB_FLAG_DEVICE_LAUNCH) && c->slabs.size() > 1) {
+    for (auto &s : c->slabs)
+      if (s.device != c->slabs[0].device)
+        return fail(IB_EINVAL, "device-launch graphs must live on one device");
+  }
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_TRY(sync_all(c));
+  free_graphs(c);
+  c->K = batch_size;
+  c->gflags = flags;
+  c->gmode = build_mode;
+  ib_times t = {};
+  size_t f0 = 0, f1 = 0, tot = 0;
+  IB_CUDA(cudaMemGetInfo(&f0, &tot));
+  int rc = build_one(c, c->cur, &t);
+  if (rc == IB_OK && c->ping_pong() && (batch_size & 1)) rc = build_one(c, c->cur ^ 1, &t);
+  if (rc != IB_OK) {
+    std::string msg = g_err;
+    free_graphs(c);
+    g_err = msg;
+    return rc;
+  }
+  IB_CUDA(cudaMemGetInfo(&f1, &tot));
+  t.graph_bytes = (int64_t)f0 - (int64_t)f1;
+  if (tm) *tm = t;
+  return IB_OK;
+}
+
+int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
+  IB_TRY(check_ctx(c));
+  if (num_batches < 0) return fail(IB_EINVAL, "num_batches must be >= 0");
+  if (c->K < 1) return fail(IB_ESTATE, "no graph built: call ib_graph_build first");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_TRY(sync_all(c));
+  ib_times t = {};
+  // the state parity may have moved since the build (e.g. an odd stream run): build lazily
+  if (!c->exec[c->cur]) IB_TRY(build_one(c, c->cur, &t));
+  if (c->ping_pong() && (c->K & 1) && !c->exec[c->cur ^ 1]) IB_TRY(build_one(c, c->cur ^ 1, &t));
+  const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
+  const int64_t per = c->K * (c->solver == IB_SOLVER_FDTD ? 2 : (int64_t)c->slabs.size());
+  auto a = clk::now();
+  IB_CUDA(cudaEventRecord(c->t0, c->stream()));
+  if (num_batches > 0) {
+    if (wh) {
+      if (c->ping_pong() && (c->K & 1) && num_batches > 1)
+        return fail(IB_EINVAL, "IB_FLAG_WHILE with an odd batch_size needs num_batches <= 1 (ping-pong parity)");
+      int nb = (int)num_batches;
+      IB_CUDA(cudaMemcpyAsync(c->d_counter, &nb, sizeof(int), cudaMemcpyHostToDevice, c->stream()));
+      IB_CUDA(cudaGraphLaunch(c->exec[c->cur], c->stream()));
+      t.launches = 1;
+      if (c->ping_pong() && (c->K & 1)) c->cur ^= 1;
+    } else {
+      for (int64_t b = 0; b < num_batches; ++b) {
+        IB_CUDA(cudaGraphLaunch(c->exec[c->cur], c->stream()));
+        if (c->ping_pong() && (c->K & 1)) c->cur ^= 1;
+      }
+      t.launches = num_batches;
+    }
+  }
+  IB_CUDA(cudaEventRecord(c->t1, c->stream()));
+  IB_CUDA(cudaEventSynchronize(c->t1));
+  auto b = clk::now();
+  float ms = 0;
+  IB_CUDA(cudaEventElapsedTime(&ms, c->t0, c->t1));
+  t.exec_s = secs(a, b);
+  t.gpu_s = ms * 1e-3;
+  t.kernels = per * num_batches;
+  if (tm) *tm = t;
+  return IB_OK;
+}
+
+int ib_host_alloc(void **ptr, size_t bytes) {
+  if (!ptr) return fail(IB_EINVAL, "ptr is null");
+  IB_CUDA(cudaMallocHost(ptr, bytes ? bytes : 1));
+  return IB_OK;
+}
+
+int ib_host_free(void *ptr) {
+  if (ptr) IB_CUDA(cudaFreeHost(ptr));
+  return IB_OK;
+}
+
+uint64_t ib_fnv1a64(const void *data, size_t nbytes, uint64_t h) {
+  const unsigned char *p = (const unsigned char *)data;
+  for (size_t i = 0; i < nbytes; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+uint64_t ib_fnv1a64_f64(const void *values, size_t n, int dtype, uint64_t h) {
+  if (dtype == IB_F64) return ib_fnv1a64(values, n * 8, h);
+  const float *f = (const float *)values;
+  for (size_t i = 0; i < n; ++i) {
+    const double d = (double)f[i];
+    unsigned char b[8];
+    std::memcpy(b, &d, 8);  // x86-64 is little-endian: these are the "<f8" bytes
+    for (int q = 0; q < 8; ++q) {
+      h ^= b[q];
+      h *= 0x100000001b3ULL;
+    }
+  }
+  return h;
+}
+
+int ib_flush_l2(ib_ctx *c) {
+  IB_TRY(check_ctx(c));
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  if (!c->flush) {
+    int dev = c->slabs[0].device, l2 = 0;
+    IB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    c->flush_bytes = std::max<size_t>((size_t)l2 * 2, 256u << 20);
+    IB_CUDA(cudaMalloc(&c->flush, c->flush_bytes));
+  }
+  static uint32_t salt = 1;
+  const int64_t n16 = (int64_t)(c->flush_bytes / 16);
+  ib::k_flush<<<148 * 4, 512, 0, c->stream()>>>((uint4 *)c->flush, n16, salt++);
+  IB_CUDA(cudaGetLastError());
+  IB_CUDA(cudaStreamSynchronize(c->stream()));
+  return IB_OK;
+}
+
+}  // extern "C"
