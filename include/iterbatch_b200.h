@@ -127,6 +127,11 @@ int ib_num_steps(const ib_ctx *ctx);
 int ib_graph_build(ib_ctx *ctx, int64_t batch_size, int build_mode, int flags, ib_times *times);
 int ib_graph_run(ib_ctx *ctx, int64_t num_batches, ib_times *times);
 int ib_graph_destroy(ib_ctx *ctx);
+/* run_batched in one call: build (T_C) + num_batches launches (T_E) + destroy. times->gpu_s is
+ * the CUDA-event interval from before the build to the end of the last kernel, i.e. the paper's
+ * total T = T_C + T_E (Eq. 1) on the device clock; build_s / exec_s split it on the host clock. */
+int ib_run_batched(ib_ctx *ctx, int64_t batch_size, int64_t num_batches, int build_mode,
+                   int flags, ib_times *times);
 int64_t ib_graph_batch_size(const ib_ctx *ctx);
 
 /* Device synchronisation of the context's streams. */

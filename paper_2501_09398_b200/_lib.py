@@ -68,6 +68,7 @@ PROTOTYPES = [
     ("ib_graph_build", _I, [_P, _I64, _I, _I, _T]),
     ("ib_graph_run", _I, [_P, _I64, _T]),
     ("ib_graph_destroy", _I, [_P]),
+    ("ib_run_batched", _I, [_P, _I64, _I64, _I, _I, _T]),
     ("ib_graph_batch_size", _I64, [_P]),
     ("ib_sync", _I, [_P]),
     ("ib_host_alloc", _I, [ctypes.POINTER(_P), _SZ]),

@@ -949,6 +949,40 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
   return IB_OK;
 }
 
+int ib_run_batched(ib_ctx *c, int64_t batch_size, int64_t num_batches, int build_mode, int flags,
+                   ib_times *tm) {
+  IB_TRY(check_ctx(c));
+  if (batch_size < 1) return fail(IB_EINVAL, "batch_size must be >= 1");
+  if (num_batches < 0) return fail(IB_EINVAL, "num_batches must be >= 0");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_TRY(sync_all(c));
+  cudaEvent_t e0;
+  IB_CUDA(cudaEventCreate(&e0));
+  IB_CUDA(cudaEventRecord(e0, c->stream()));
+  ib_times b = {}, r = {};
+  int rc = ib_graph_build(c, batch_size, build_mode, flags, &b);
+  if (rc == IB_OK) rc = ib_graph_run(c, num_batches, &r);
+  if (rc != IB_OK) {
+    cudaEventDestroy(e0);
+    return rc;
+  }
+  float ms = 0;
+  cudaError_t e = cudaEventElapsedTime(&ms, e0, c->t1);
+  cudaEventDestroy(e0);
+  IB_CUDA(e);
+  free_graphs(c);
+  if (tm) {
+    *tm = b;
+    tm->exec_s = r.exec_s;
+    tm->gpu_s = ms * 1e-3;
+    tm->kernels = r.kernels;
+    tm->launches = r.launches;
+    tm->build_s += r.build_s;  // lazily built parity executables, if any
+  }
+  return IB_OK;
+}
+
 int ib_host_alloc(void **ptr, size_t bytes) {
   if (!ptr) return fail(IB_EINVAL, "ptr is null");
   IB_CUDA(cudaMallocHost(ptr, bytes ? bytes : 1));

@@ -443,6 +443,15 @@ class DeviceSolver:
         self.batch_size = int(batch_size)
         return Times.from_c(t)
 
+    def run_batched(self, batch_size: int, num_batches: int, build: str = "manual",
+                    pdl: bool = False, while_loop: bool = False) -> Times:
+        """Build + replay + destroy in one call; ``gpu_s`` is T = T_C + T_E on the device clock."""
+        flags = (_lib.FLAG_PDL if pdl else 0) | (_lib.FLAG_WHILE if while_loop else 0)
+        t = _lib.IbTimes()
+        _lib.check(_lib.lib().ib_run_batched(self.ctx, int(batch_size), int(num_batches),
+                                             _lib.BUILD[build], flags, ctypes.byref(t)))
+        return Times.from_c(t)
+
     def run_graph(self, num_batches: int) -> Times:
         t = _lib.IbTimes()
         _lib.check(_lib.lib().ib_graph_run(self.ctx, int(num_batches), ctypes.byref(t)))
