@@ -134,6 +134,252 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- vector helpers -------------------------------------------------------------------------
+template <typename T> struct vec16;
+template <> struct vec16<float> { using type = float4; static constexpr int n = 4; };
+template <> struct vec16<double> { using type = double2; static constexpr int n = 2; };
+
+template <typename T>
+__device__ __forceinline__ void ld16(T (&r)[16 / sizeof(T)], const T *p) {
+  using VT = typename vec16<T>::type;
+  const VT v = *reinterpret_cast<const VT *>(p);
+  if constexpr (sizeof(T) == 4) { r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w; }
+  else { r[0] = v.x; r[1] = v.y; }
+}
+template <typename T>
+__device__ __forceinline__ void st16(T *p, const T (&r)[16 / sizeof(T)]) {
+  using VT = typename vec16<T>::type;
+  VT v;
+  if constexpr (sizeof(T) == 4) { v.x = r[0]; v.y = r[1]; v.z = r[2]; v.w = r[3]; }
+  else { v.x = r[0]; v.y = r[1]; }
+  *reinterpret_cast<VT *>(p) = v;
+}
+
+// One Hotspot cell, the reference op order (workloads.py:182-185 / 188-204).
+template <typename T, bool D3>
+__device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T zp, T pw, T k, T loss) {
+  T sum = rn<T>::add(rn<T>::add(up, dn), rn<T>::add(ym, yp));
+  if (D3) sum = rn<T>::add(sum, rn<T>::add(zm, zp));
+  const T q = rn<T>::sub(sum, rn<T>::mul(loss, c));
+  return rn<T>::add(rn<T>::add(c, rn<T>::mul(k, q)), pw);
+}
+
+// ================================================================================================
+// Hotspot, vectorised one-row-per-thread variant for L2-resident grids (the launch-bound configs).
+// A thread owns V = 16/sizeof(T) consecutive cells of one plane row (one 16-byte load/store); all
+// of its loads are independent, so the whole grid's reads are in flight at once — no marching
+// chain. Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles
+// a y-row). grid = (ceil(M/V/256), rows).
+// ================================================================================================
+template <typename T, bool D3>
+__global__ void __launch_bounds__(256)
+    k_hotspot_vec(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
+                  int rows, int C, int L, T k, T loss, int has_top, int has_bot,
+                  T *__restrict__ halo_up, T *__restrict__ halo_dn) {
+  constexpr int V = 16 / sizeof(T);
+  pdl_trigger();
+  const int64_t M = (int64_t)C * L;
+  const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
+  const int i = blockIdx.y;
+  pdl_wait();
+  if (m >= M) return;
+  const T *s = src + (int64_t)i * M + m;
+  T c[V], up[V], dn[V], ym[V], yp[V], pw[V];
+  ld16<T>(c, s);
+  if (i > 0 || has_top) ld16<T>(up, s - M); else for (int e = 0; e < V; ++e) up[e] = c[e];
+  if (i + 1 < rows || has_bot) ld16<T>(dn, s + M); else for (int e = 0; e < V; ++e) dn[e] = c[e];
+  ld16<T>(pw, power + (int64_t)i * M + m);
+  T out[V];
+  if (D3) {
+    const int j = (int)(m / L);
+    const int l = (int)(m - (int64_t)j * L);
+    if (j > 0) ld16<T>(ym, s - L); else for (int e = 0; e < V; ++e) ym[e] = c[e];
+    if (j < C - 1) ld16<T>(yp, s + L); else for (int e = 0; e < V; ++e) yp[e] = c[e];
+    const T zl = l > 0 ? s[-1] : c[0];
+    const T zr = l + V < L ? s[V] : c[V - 1];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const T zm = e > 0 ? c[e - 1] : zl;
+      const T zp = e < V - 1 ? c[e + 1] : zr;
+      out[e] = hotspot_cell<T, true>(up[e], c[e], dn[e], ym[e], yp[e], zm, zp, pw[e], k, loss);
+    }
+  } else {
+    const T yl = m > 0 ? s[-1] : c[0];
+    const T yr = m + V < M ? s[V] : c[V - 1];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const T a = e > 0 ? c[e - 1] : yl;
+      const T b = e < V - 1 ? c[e + 1] : yr;
+      out[e] = hotspot_cell<T, false>(up[e], c[e], dn[e], a, b, T(0), T(0), pw[e], k, loss);
+    }
+  }
+  st16<T>(dst + (int64_t)i * M + m, out);
+  if (i == 0 && halo_up) st16<T>(halo_up + m, out);
+  if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
+}
+
+// ---- bulk-copy (TMA) + mbarrier primitives ------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion signalled on the mbarrier as tx bytes.
+// dst, src and bytes must be 16-byte aligned / multiples of 16.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ================================================================================================
+// Hotspot, TMA-pipelined plane march for HBM-bound grids (Hotspot3D 2048x2048x256).
+// A CTA owns a tile of TM = G*V*256 consecutive plane elements (whole y-rows in 3-D) and a chunk
+// of rows along axis 0. One elected thread streams each plane's tile (+ one y-row halo each side)
+// and the matching power tile into an NS-stage shared-memory ring with cp.async.bulk, completion
+// tracked by one mbarrier per stage; NS-1 planes are in flight while the CTA computes. The x-1/x
+// planes live in registers (march), the x+1 plane and the y/z neighbours are read from shared
+// memory. Stores are 16-byte vector stores straight to global. Requirements (else the vec kernel
+// runs): M % V == 0, 3-D: L % V == 0 and TM % L == 0.
+// ================================================================================================
+template <typename T, bool D3, int G>
+__global__ void __launch_bounds__(256)
+    k_hotspot_tma(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
+                  int rows, int C, int L, int rows_per_cta, int nstages, T k, T loss, int has_top,
+                  int has_bot, T *__restrict__ halo_up, T *__restrict__ halo_dn) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int TM = G * V * 256;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  pdl_trigger();
+  const int64_t M = (int64_t)C * L;
+  const int H = D3 ? L : V;  // y-halo (3-D: one y-row; 2-D: one 16-byte group)
+  const int64_t m0 = (int64_t)blockIdx.x * TM;
+  const int64_t m1 = min(M, m0 + TM);
+  const int64_t lo = max((int64_t)0, m0 - H);
+  const int64_t hi = min(M, m1 + H);
+  const int cap = TM + 2 * H;  // T elements per stage
+  T *ringT = reinterpret_cast<T *>(smem_raw);
+  T *ringP = ringT + (size_t)nstages * cap;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ringP + (size_t)nstages * TM);
+  const int i0 = blockIdx.y * rows_per_cta;
+  const int i1 = min(rows, i0 + rows_per_cta);
+  const int n_out = i1 - i0;
+  const int n_load = n_out + 2;  // planes i0-1 .. i1
+  const int qlo = has_top ? -1 : 0, qhi = has_bot ? rows : rows - 1;
+  const uint32_t bytesT = (uint32_t)((hi - lo) * sizeof(T));
+  const uint32_t bytesP = (uint32_t)((m1 - m0) * sizeof(T));
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < nstages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();  // from here on the previous kernel's writes are visible
+  auto issue = [&](int t) {
+    const int s = t % nstages;
+    int q = i0 - 1 + t;
+    const bool out_row = (t >= 1 && t <= n_out);
+    q = q < qlo ? qlo : (q > qhi ? qhi : q);
+    mbar_expect_tx(&bar[s], bytesT + (out_row ? bytesP : 0u));
+    bulk_g2s(ringT + (size_t)s * cap, src + (int64_t)q * M + lo, bytesT, &bar[s]);
+    if (out_row)
+      bulk_g2s(ringP + (size_t)s * TM, power + (int64_t)(i0 - 1 + t) * M + m0, bytesP, &bar[s]);
+  };
+  if (tid == 0)
+    for (int t = 0; t < min(nstages, n_load); ++t) issue(t);
+
+  T up[G][V], cu[G][V];
+  // planes t=0 (x-1 of the first output row) and t=1 (first output row) into registers
+  mbar_wait(&bar[0], 0);
+  mbar_wait(&bar[1 % nstages], (1 / nstages) & 1);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int64_t m = m0 + ((int64_t)g * 256 + tid) * V;
+    if (m < m1) {
+      ld16<T>(up[g], ringT + (m - lo));
+      ld16<T>(cu[g], ringT + (size_t)(1 % nstages) * cap + (m - lo));
+    }
+  }
+  __syncthreads();  // stage of t=0 is free
+  if (tid == 0 && nstages < n_load) {
+    fence_proxy_async();
+    issue(nstages);
+  }
+  for (int u = 0; u < n_out; ++u) {
+    const int i = i0 + u;
+    const int tc = u + 1, td = u + 2;
+    const T *pc = ringT + (size_t)(tc % nstages) * cap - lo;  // index with global m
+    const T *pd = ringT + (size_t)(td % nstages) * cap - lo;
+    const T *pp = ringP + (size_t)(tc % nstages) * TM - m0;
+    mbar_wait(&bar[td % nstages], (td / nstages) & 1);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t m = m0 + ((int64_t)g * 256 + tid) * V;
+      if (m >= m1) continue;
+      T dn[V], ym[V], yp[V], pw[V], out[V];
+      ld16<T>(dn, pd + m);
+      ld16<T>(pw, pp + m);
+      if (D3) {
+        const int j = (int)(m / L);
+        const int l = (int)(m - (int64_t)j * L);
+        if (j > 0) ld16<T>(ym, pc + m - L); else for (int e = 0; e < V; ++e) ym[e] = cu[g][e];
+        if (j < C - 1) ld16<T>(yp, pc + m + L); else for (int e = 0; e < V; ++e) yp[e] = cu[g][e];
+        const T zl = l > 0 ? pc[m - 1] : cu[g][0];
+        const T zr = l + V < L ? pc[m + V] : cu[g][V - 1];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const T zm = e > 0 ? cu[g][e - 1] : zl;
+          const T zp = e < V - 1 ? cu[g][e + 1] : zr;
+          out[e] = hotspot_cell<T, true>(up[g][e], cu[g][e], dn[e], ym[e], yp[e], zm, zp, pw[e], k, loss);
+        }
+      } else {
+        const T yl = m > 0 ? pc[m - 1] : cu[g][0];
+        const T yr = m + V < M ? pc[m + V] : cu[g][V - 1];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const T a = e > 0 ? cu[g][e - 1] : yl;
+          const T b = e < V - 1 ? cu[g][e + 1] : yr;
+          out[e] = hotspot_cell<T, false>(up[g][e], cu[g][e], dn[e], a, b, T(0), T(0), pw[e], k, loss);
+        }
+      }
+      T *o = dst + (int64_t)i * M + m;
+      st16<T>(o, out);
+      if (i == 0 && halo_up) st16<T>(halo_up + m, out);
+      if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        up[g][e] = cu[g][e];
+        cu[g][e] = dn[e];
+      }
+    }
+    __syncthreads();  // everyone is done with the stage of plane tc
+    const int tn = tc + nstages;
+    if (tid == 0 && tn < n_load) {
+      fence_proxy_async();
+      issue(tn);
+    }
+  }
+}
+
 // ================================================================================================
 // FDTD Yee leapfrog, fields in place.  workloads.py:325-413
 // Shapes for (nx, ny, nz) cells:  ex (nx,ny+1,nz+1) ey (nx+1,ny,nz+1) ez (nx+1,ny+1,nz)
@@ -244,6 +490,205 @@ __global__ void __launch_bounds__(256)
       ez[e] = zero;
     }
   }
+}
+
+// ================================================================================================
+// FDTD, x-marching variants. One thread per (j,k) point of the unified (ny+1) x (nz+1) plane walks
+// a chunk of x-planes: all index arithmetic is done once, every step only advances six pointers
+// by their plane strides, and the x-neighbours the update re-reads (ey/ez at i for H, hz/hy at
+// i-1 for E) are carried in registers from the previous step. Same arithmetic as k_fdtd_h/_e.
+// grid = (ceil((ny+1)(nz+1)/256), ceil(planes / planes_per_cta)).
+// ================================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_fdtd_h_march(const T *__restrict__ ex, const T *__restrict__ ey, const T *__restrict__ ez,
+                   T *__restrict__ hx, T *__restrict__ hy, T *__restrict__ hz, int nx, int ny, int nz,
+                   int planes_per_cta, T c_h, T d, int unit_d) {
+  pdl_trigger();
+  const int pw = nz + 1;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i0 = blockIdx.y * planes_per_cta;
+  const int i1 = min(nx + 1, i0 + planes_per_cta);
+  pdl_wait();
+  if (p >= (ny + 1) * pw) return;
+  const int j = p / pw;
+  const int k = p - j * pw;
+  const bool ud = unit_d != 0;
+  const bool bx = j < ny && k < nz, by = k < nz, bz = j < ny;
+  const int64_t exs = (int64_t)(ny + 1) * (nz + 1), eys = (int64_t)ny * (nz + 1), ezs = (int64_t)(ny + 1) * nz;
+  const int64_t hxs = (int64_t)ny * nz, hys = (int64_t)(ny + 1) * nz, hzs = (int64_t)ny * (nz + 1);
+  const T *pex = ex + i0 * exs + (int64_t)j * (nz + 1) + k;
+  const T *pey = ey + i0 * eys + (int64_t)j * (nz + 1) + k;
+  const T *pez = ez + i0 * ezs + (int64_t)j * nz + k;
+  T *phx = hx + i0 * hxs + (int64_t)j * nz + k;
+  T *phy = hy + i0 * hys + (int64_t)j * nz + k;
+  T *phz = hz + i0 * hzs + (int64_t)j * (nz + 1) + k;
+  T ey_c = bz ? pey[0] : T(0);  // ey[i][j][k]
+  T ez_c = by ? pez[0] : T(0);  // ez[i][j][k]
+  for (int i = i0; i < i1; ++i) {
+    if (bx) *phx = curl_update<T>(*phx, c_h, pey[1], ey_c, pez[nz], ez_c, d, ud);
+    if (i < nx) {
+      const T ez_n = by ? pez[ezs] : T(0);  // ez[i+1][j][k]
+      const T ey_n = bz ? pey[eys] : T(0);  // ey[i+1][j][k]
+      const T exc = pex[0];
+      if (by) *phy = curl_update<T>(*phy, c_h, ez_n, ez_c, pex[1], exc, d, ud);
+      if (bz) *phz = curl_update<T>(*phz, c_h, pex[nz + 1], exc, ey_n, ey_c, d, ud);
+      ey_c = ey_n;
+      ez_c = ez_n;
+    }
+    pex += exs; pey += eys; pez += ezs;
+    phx += hxs; phy += hys; phz += hzs;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_fdtd_e_march(T *__restrict__ ex, T *__restrict__ ey, T *__restrict__ ez,
+                   const T *__restrict__ hx, const T *__restrict__ hy, const T *__restrict__ hz,
+                   int nx, int ny, int nz, int planes_per_cta, T c_e, T d, int unit_d) {
+  pdl_trigger();
+  const int pw = nz + 1;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i0 = blockIdx.y * planes_per_cta;
+  const int i1 = min(nx + 1, i0 + planes_per_cta);
+  pdl_wait();
+  if (p >= (ny + 1) * pw) return;
+  const int j = p / pw;
+  const int k = p - j * pw;
+  const bool ud = unit_d != 0;
+  const int64_t exs = (int64_t)(ny + 1) * (nz + 1), eys = (int64_t)ny * (nz + 1), ezs = (int64_t)(ny + 1) * nz;
+  const int64_t hxs = (int64_t)ny * nz, hys = (int64_t)(ny + 1) * nz, hzs = (int64_t)ny * (nz + 1);
+  T *pex = ex + i0 * exs + (int64_t)j * (nz + 1) + k;
+  T *pey = ey + i0 * eys + (int64_t)j * (nz + 1) + k;
+  T *pez = ez + i0 * ezs + (int64_t)j * nz + k;
+  const T *phx = hx + i0 * hxs + (int64_t)j * nz + k;
+  const T *phy = hy + i0 * hys + (int64_t)j * nz + k;
+  const T *phz = hz + i0 * hzs + (int64_t)j * (nz + 1) + k;
+  const bool jin = j >= 1 && j <= ny - 1, kin = k >= 1 && k <= nz - 1;
+  const bool ex_upd = jin && kin;   // ex interior in (j,k)
+  const bool ey_col = j < ny, ez_col = k < nz;
+  // hz[i-1][j][k] and hy[i-1][j][k], carried down the march
+  T hz_p = (i0 >= 1 && i0 - 1 < nx && j < ny) ? phz[-hzs] : T(0);
+  T hy_p = (i0 >= 1 && i0 - 1 < nx && k < nz) ? phy[-hys] : T(0);
+  const T zero = T(0);
+  for (int i = i0; i < i1; ++i) {
+    const bool iin = i >= 1 && i <= nx - 1;
+    const T hz_c = (i < nx && j < ny) ? phz[0] : zero;
+    const T hy_c = (i < nx && k < nz) ? phy[0] : zero;
+    if (i < nx)
+      *pex = ex_upd ? curl_update<T>(*pex, c_e, hz_c, phz[-(nz + 1)], hy_c, phy[-1], d, ud) : zero;
+    if (ey_col)
+      *pey = (iin && kin) ? curl_update<T>(*pey, c_e, phx[0], phx[-1], hz_c, hz_p, d, ud) : zero;
+    if (ez_col)
+      *pez = (iin && jin) ? curl_update<T>(*pez, c_e, hy_c, hy_p, phx[0], phx[-nz], d, ud) : zero;
+    hz_p = hz_c;
+    hy_p = hy_c;
+    pex += exs; pey += eys; pez += ezs;
+    phx += hxs; phy += hys; phz += hzs;
+  }
+}
+
+// ================================================================================================
+// FDTD, lean lattice kernels (default). block = (32 along z, 8 along y), grid = (z-tiles, y-tiles,
+// nx+1): no integer division, 32-bit offsets (the launch layer checks every field has < 2^31
+// elements), and the cell size folded in at compile time (UNIT_D: /d skipped, exact for d == 1).
+// Every load of a thread is independent, so a fully occupied SM keeps ~12 loads per thread in
+// flight. Offsets: A = ex-shaped (ny+1, nz+1) rows, B = (ny, nz+1) rows (ey, hz),
+//                  Cc = (ny+1, nz) rows (ez, hy), D = (ny, nz) rows (hx).
+// ================================================================================================
+// Compiler barrier that needs its operands in registers: every load feeding it is issued before
+// it, so independent loads are in flight together instead of being sunk into the branches that
+// consume them (ptxas otherwise serialises the three guarded updates' loads).
+__device__ __forceinline__ void pin(float v) { asm volatile("" ::"f"(v)); }
+__device__ __forceinline__ void pin(double v) { asm volatile("" ::"d"(v)); }
+template <typename T, typename... R>
+__device__ __forceinline__ void pin(T v, R... r) {
+  pin(v);
+  pin(r...);
+}
+
+template <typename T, bool UNIT_D>
+__device__ __forceinline__ T curl2(T f, T c, T p, T q, T r, T s, T d) {
+  T a = rn<T>::sub(p, q);
+  T b = rn<T>::sub(r, s);
+  if (!UNIT_D) {
+    a = rn<T>::div(a, d);
+    b = rn<T>::div(b, d);
+  }
+  return rn<T>::add(f, rn<T>::mul(c, rn<T>::sub(a, b)));
+}
+
+template <typename T, bool UNIT_D>
+__global__ void __launch_bounds__(256)
+    k_fdtd_h2(const T *__restrict__ ex, const T *__restrict__ ey, const T *__restrict__ ez,
+              T *__restrict__ hx, T *__restrict__ hy, T *__restrict__ hz, int nx, int ny, int nz,
+              T c_h, T d) {
+  pdl_trigger();
+  const int k = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  const int i = blockIdx.z;
+  pdl_wait();
+  if (k > nz || j > ny) return;
+  const int nz1 = nz + 1, ny1 = ny + 1;
+  const int A = (i * ny1 + j) * nz1 + k;
+  const int B = (i * ny + j) * nz1 + k;
+  const int Cc = (i * ny1 + j) * nz + k;
+  const int D = (i * ny + j) * nz + k;
+  const bool ux = j < ny && k < nz;  // hx[i,j,k] (i <= nx always)
+  const bool uy = i < nx && k < nz;  // hy[i,j,k]
+  const bool uz = i < nx && j < ny;  // hz[i,j,k]
+  // issue every load before any use: ~12 independent loads in flight per thread
+  const T hx0 = ux ? hx[D] : T(0), hy0 = uy ? hy[Cc] : T(0), hz0 = uz ? hz[B] : T(0);
+  const T ey_b = (ux || uz) ? ey[B] : T(0);
+  const T ey_k = ux ? ey[B + 1] : T(0);
+  const T ey_i = uz ? ey[B + ny * nz1] : T(0);
+  const T ez_c = (ux || uy) ? ez[Cc] : T(0);
+  const T ez_j = ux ? ez[Cc + nz] : T(0);
+  const T ez_i = uy ? ez[Cc + ny1 * nz] : T(0);
+  const T ex_a = (uy || uz) ? ex[A] : T(0);
+  const T ex_k = uy ? ex[A + 1] : T(0);
+  const T ex_j = uz ? ex[A + nz1] : T(0);
+  pin(hx0, hy0, hz0, ey_b, ey_k, ey_i, ez_c, ez_j, ez_i, ex_a, ex_k, ex_j);
+  if (ux) hx[D] = curl2<T, UNIT_D>(hx0, c_h, ey_k, ey_b, ez_j, ez_c, d);   // ey(k+1)-ey, ez(j+1)-ez
+  if (uy) hy[Cc] = curl2<T, UNIT_D>(hy0, c_h, ez_i, ez_c, ex_k, ex_a, d);  // ez(i+1)-ez, ex(k+1)-ex
+  if (uz) hz[B] = curl2<T, UNIT_D>(hz0, c_h, ex_j, ex_a, ey_i, ey_b, d);   // ex(j+1)-ex, ey(i+1)-ey
+}
+
+template <typename T, bool UNIT_D>
+__global__ void __launch_bounds__(256)
+    k_fdtd_e2(T *__restrict__ ex, T *__restrict__ ey, T *__restrict__ ez, const T *__restrict__ hx,
+              const T *__restrict__ hy, const T *__restrict__ hz, int nx, int ny, int nz, T c_e, T d) {
+  pdl_trigger();
+  const int k = blockIdx.x * 32 + threadIdx.x;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  const int i = blockIdx.z;
+  pdl_wait();
+  if (k > nz || j > ny) return;
+  const int nz1 = nz + 1, ny1 = ny + 1;
+  const int A = (i * ny1 + j) * nz1 + k;
+  const int B = (i * ny + j) * nz1 + k;
+  const int Cc = (i * ny1 + j) * nz + k;
+  const int D = (i * ny + j) * nz + k;
+  const bool iin = i >= 1 && i < nx, jin = j >= 1 && j < ny, kin = k >= 1 && k < nz;
+  const bool wx = i < nx, wy = j < ny, wz = k < nz;  // the component exists here
+  const bool ux = wx && jin && kin;                   // interior: updated (else wall: written 0)
+  const bool uy = wy && iin && kin;
+  const bool uz = wz && iin && jin;
+  const T ex0 = ux ? ex[A] : T(0), ey0 = uy ? ey[B] : T(0), ez0 = uz ? ez[Cc] : T(0);
+  const T hz_b = (ux || uy) ? hz[B] : T(0);
+  const T hz_j = ux ? hz[B - nz1] : T(0);
+  const T hz_i = uy ? hz[B - ny * nz1] : T(0);
+  const T hy_c = (ux || uz) ? hy[Cc] : T(0);
+  const T hy_k = ux ? hy[Cc - 1] : T(0);
+  const T hy_i = uz ? hy[Cc - ny1 * nz] : T(0);
+  const T hx_d = (uy || uz) ? hx[D] : T(0);
+  const T hx_k = uy ? hx[D - 1] : T(0);
+  const T hx_j = uz ? hx[D - nz] : T(0);
+  pin(ex0, ey0, ez0, hz_b, hz_j, hz_i, hy_c, hy_k, hy_i, hx_d, hx_k, hx_j);
+  const T zero = T(0);
+  if (wx) ex[A] = ux ? curl2<T, UNIT_D>(ex0, c_e, hz_b, hz_j, hy_c, hy_k, d) : zero;  // hz(j)-hz(j-1), hy(k)-hy(k-1)
+  if (wy) ey[B] = uy ? curl2<T, UNIT_D>(ey0, c_e, hx_d, hx_k, hz_b, hz_i, d) : zero;  // hx(k)-hx(k-1), hz(i)-hz(i-1)
+  if (wz) ez[Cc] = uz ? curl2<T, UNIT_D>(ez0, c_e, hy_c, hy_i, hx_d, hx_j, d) : zero; // hy(i)-hy(i-1), hx(j)-hx(j-1)
 }
 
 // ---- utilities ---------------------------------------------------------------------------------

@@ -66,6 +66,7 @@ struct DeviceGuard {
 struct Launch {
   const void *func = nullptr;
   dim3 grid, block;
+  size_t smem = 0;  // dynamic shared memory bytes
   int slab = 0;
   int nargs = 0;
   alignas(16) unsigned char slot[16][16];
@@ -109,6 +110,11 @@ struct Slab {
   int rows() const { return row_hi - row_lo; }
 };
 
+const char *env_str(const char *name) {
+  const char *v = std::getenv(name);
+  return (v && *v) ? v : nullptr;
+}
+
 int64_t env_int(const char *name, int64_t dflt) {
   const char *v = std::getenv(name);
   if (!v || !*v) return dflt;
@@ -128,6 +134,7 @@ struct ib_ctx {
   int fndim[6] = {};
   int nfields = 0;
   int cur = 0;              // hotspot ping-pong parity: buf[cur] holds the current temperature
+  int num_sms = 148;        // of slab 0's device
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   cudaStream_t cap_stream = nullptr;  // used only for stream capture of single-slab graphs
   // graph state
@@ -170,21 +177,67 @@ int hotspot_rows_per_chunk(const ib_ctx *c, int rows) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(rpc, rows));
 }
 
+// Kernel variant for a hotspot grid. IB_HOTSPOT_KERNEL=scalar|vec|tma forces one (if legal).
+//   vec    one 16-byte group per thread, every load independent: best for L2-resident grids
+//   tma    cp.async.bulk plane-march pipeline: best once the state no longer fits in L2
+//   scalar marching fallback for shapes the vector paths cannot take (M or L not a multiple of V)
+enum class HotKernel { Scalar, Vec, Tma };
+
+template <typename T>
+int tma_groups(const ib_ctx *c) {  // G such that TM = G*V*256 holds whole y-rows; 0 = not possible
+  constexpr int V = 16 / sizeof(T);
+  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
+  const int64_t L = d3 ? c->dims[2] : 1;
+  for (int G : {2, 1, 4}) {
+    const int64_t TM = (int64_t)G * V * 256;
+    if (!d3 || (TM % L == 0 && L <= 1024)) return G;
+  }
+  return 0;
+}
+
+template <typename T>
+HotKernel hotspot_variant(const ib_ctx *c, int rows) {
+  constexpr int V = 16 / sizeof(T);
+  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
+  const int64_t M = c->plane();
+  const int64_t L = d3 ? c->dims[2] : 1;
+  const bool vec_ok = (M % V == 0) && (!d3 || L % V == 0) && rows <= 65535;
+  const bool tma_ok = vec_ok && tma_groups<T>(c) > 0 && rows >= 2;
+  const char *force = env_str("IB_HOTSPOT_KERNEL");
+  if (force) {
+    if (!std::strcmp(force, "tma") && tma_ok) return HotKernel::Tma;
+    if (!std::strcmp(force, "vec") && vec_ok) return HotKernel::Vec;
+    if (!std::strcmp(force, "scalar")) return HotKernel::Scalar;
+  }
+  const int64_t state_bytes = 3 * M * c->dims[0] * (int64_t)sizeof(T);
+  if (tma_ok && state_bytes >= (96LL << 20)) return HotKernel::Tma;
+  if (vec_ok) return HotKernel::Vec;
+  return HotKernel::Scalar;
+}
+
+template <typename T, bool D3>
+const void *tma_fn(int G) {
+  switch (G) {
+    case 1: return (const void *)ib::k_hotspot_tma<T, D3, 1>;
+    case 4: return (const void *)ib::k_hotspot_tma<T, D3, 4>;
+    default: return (const void *)ib::k_hotspot_tma<T, D3, 2>;
+  }
+}
+
 template <typename T>
 void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  constexpr int V = 16 / sizeof(T);
   const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
   const int C = (int)c->dims[1];
   const int L = d3 ? (int)c->dims[2] : 1;
   const int64_t plane = c->plane();
   const T k = (T)c->scalars[0];
   const T loss = (T)(2.0 * (d3 ? 3 : 2));
-  const void *fn = d3 ? (const void *)ib::k_hotspot<T, true> : (const void *)ib::k_hotspot<T, false>;
   const int P = (int)c->slabs.size();
   const bool multi = P > 1;
   for (int g = 0; g < P; ++g) {
     Slab &s = c->slabs[g];
     const int rows = s.rows();
-    const int rpc = hotspot_rows_per_chunk(c, rows);
     const int64_t off = multi ? plane : 0;  // first owned plane
     const T *src = (const T *)s.buf[parity] + off;
     T *dst = (T *)s.buf[parity ^ 1] + off;
@@ -197,10 +250,46 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
       Slab &n = c->slabs[g + 1];
       dn = (T *)n.buf[parity ^ 1];
     }
+    const int top = (int)s.has_top, bot = (int)s.has_bot;
     dim3 block(256);
-    dim3 grid((unsigned)((plane + 255) / 256), (unsigned)((rows + rpc - 1) / rpc));
-    out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, rpc, k,
-                              loss, (int)s.has_top, (int)s.has_bot, up, dn));
+    switch (hotspot_variant<T>(c, rows)) {
+      case HotKernel::Vec: {
+        const void *fn = d3 ? (const void *)ib::k_hotspot_vec<T, true> : (const void *)ib::k_hotspot_vec<T, false>;
+        dim3 grid((unsigned)((plane / V + 255) / 256), (unsigned)rows);
+        out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, k, loss,
+                                  top, bot, up, dn));
+        break;
+      }
+      case HotKernel::Tma: {
+        const int G = tma_groups<T>(c);
+        const int TM = G * V * 256;
+        const int H = d3 ? L : V;
+        const int ns = (int)std::max<int64_t>(3, std::min<int64_t>(8, env_int("IB_TMA_STAGES", 4)));
+        const size_t smem = (size_t)ns * (TM + 2 * H + TM) * sizeof(T) + (size_t)ns * 8;
+        const void *fn = d3 ? tma_fn<T, true>(G) : tma_fn<T, false>(G);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t tiles = (plane + TM - 1) / TM;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+        const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
+        int64_t rpc = env_int("IB_HOTSPOT_RPC", 0);
+        if (rpc <= 0) rpc = std::max<int64_t>(16, std::min<int64_t>(128, (int64_t)rows * tiles / (12 * slots)));
+        rpc = std::min<int64_t>(rpc, rows);
+        dim3 grid((unsigned)tiles, (unsigned)((rows + rpc - 1) / rpc));
+        Launch Lz = make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, (int)rpc, ns,
+                                k, loss, top, bot, up, dn);
+        Lz.smem = smem;
+        out.push_back(Lz);
+        break;
+      }
+      default: {
+        const void *fn = d3 ? (const void *)ib::k_hotspot<T, true> : (const void *)ib::k_hotspot<T, false>;
+        const int rpc = hotspot_rows_per_chunk(c, rows);
+        dim3 grid((unsigned)((plane + 255) / 256), (unsigned)((rows + rpc - 1) / rpc));
+        out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, rpc, k,
+                                  loss, top, bot, up, dn));
+      }
+    }
   }
 }
 
@@ -212,13 +301,46 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   T **f = (T **)c->field;
   const int64_t pl = (int64_t)(ny + 1) * (nz + 1);
   dim3 block(256);
-  dim3 grid((unsigned)((pl + 255) / 256), (unsigned)(nx + 1));
-  out.push_back(make_launch((const void *)ib::k_fdtd_h<T>, grid, block, 0, (const T *)f[0],
-                            (const T *)f[1], (const T *)f[2], f[3], f[4], f[5], nx, ny, nz, ch, d,
-                            unit));
-  out.push_back(make_launch((const void *)ib::k_fdtd_e<T>, grid, block, 0, f[0], f[1], f[2],
-                            (const T *)f[3], (const T *)f[4], (const T *)f[5], nx, ny, nz, ce, d,
-                            unit));
+  const char *force = env_str("IB_FDTD_KERNEL");
+  int64_t maxel = 0;
+  for (int q = 0; q < 6; ++q) maxel = std::max(maxel, numel(c->fshape[q], 3));
+  const bool lean_ok = maxel + (int64_t)(ny + 1) * (nz + 1) < (1LL << 31);
+  if (lean_ok && (!force || !std::strcmp(force, "lean"))) {
+    dim3 b2(32, 8);
+    dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)(nx + 1));
+    const void *fh = unit ? (const void *)ib::k_fdtd_h2<T, true> : (const void *)ib::k_fdtd_h2<T, false>;
+    const void *fe = unit ? (const void *)ib::k_fdtd_e2<T, true> : (const void *)ib::k_fdtd_e2<T, false>;
+    out.push_back(make_launch(fh, grid, b2, 0, (const T *)f[0], (const T *)f[1], (const T *)f[2], f[3],
+                              f[4], f[5], nx, ny, nz, ch, d));
+    out.push_back(make_launch(fe, grid, b2, 0, f[0], f[1], f[2], (const T *)f[3], (const T *)f[4],
+                              (const T *)f[5], nx, ny, nz, ce, d));
+    return;
+  }
+  const bool flat = force && !std::strcmp(force, "flat");
+  if (flat || pl > (1LL << 30)) {
+    dim3 grid((unsigned)((pl + 255) / 256), (unsigned)(nx + 1));
+    out.push_back(make_launch((const void *)ib::k_fdtd_h<T>, grid, block, 0, (const T *)f[0],
+                              (const T *)f[1], (const T *)f[2], f[3], f[4], f[5], nx, ny, nz, ch, d, unit));
+    out.push_back(make_launch((const void *)ib::k_fdtd_e<T>, grid, block, 0, f[0], f[1], f[2],
+                              (const T *)f[3], (const T *)f[4], (const T *)f[5], nx, ny, nz, ce, d, unit));
+    return;
+  }
+  // x-march: as many x-chunks as fill one wave of resident CTAs (each CTA then streams its chunk)
+  const int64_t bpp = (pl + 255) / 256;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)ib::k_fdtd_h_march<T>, 256, 0);
+  const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
+  int64_t chunks = std::max<int64_t>(1, slots / bpp);
+  int64_t ppc = env_int("IB_FDTD_PPC", 0);
+  if (ppc <= 0) ppc = (nx + 1 + chunks - 1) / chunks;
+  ppc = std::max<int64_t>(1, std::min<int64_t>(ppc, nx + 1));
+  dim3 grid((unsigned)bpp, (unsigned)((nx + 1 + ppc - 1) / ppc));
+  out.push_back(make_launch((const void *)ib::k_fdtd_h_march<T>, grid, block, 0, (const T *)f[0],
+                            (const T *)f[1], (const T *)f[2], f[3], f[4], f[5], nx, ny, nz, (int)ppc, ch,
+                            d, unit));
+  out.push_back(make_launch((const void *)ib::k_fdtd_e_march<T>, grid, block, 0, f[0], f[1], f[2],
+                            (const T *)f[3], (const T *)f[4], (const T *)f[5], nx, ny, nz, (int)ppc, ce,
+                            d, unit));
 }
 
 void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
@@ -258,13 +380,13 @@ void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
 
 int launch_one(Launch &L, cudaStream_t s, bool pdl) {
   if (!pdl) {
-    IB_CUDA(cudaLaunchKernel(L.func, L.grid, L.block, L.args(), 0, s));
+    IB_CUDA(cudaLaunchKernel(L.func, L.grid, L.block, L.args(), L.smem, s));
     return IB_OK;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = L.grid;
   cfg.blockDim = L.block;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = L.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -361,7 +483,7 @@ int build_manual_chain(ib_ctx *c, cudaGraph_t graph, int64_t K, int parity, bool
       np.func = const_cast<void *>(L.func);
       np.gridDim = L.grid;
       np.blockDim = L.block;
-      np.sharedMemBytes = 0;
+      np.sharedMemBytes = (unsigned)L.smem;
       np.kernelParams = L.args();
       np.extra = nullptr;
       cudaGraphNode_t node;
@@ -580,6 +702,7 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
     }
   }
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->slabs[0].device));
   IB_CUDA(cudaEventCreate(&c->t0));
   IB_CUDA(cudaEventCreate(&c->t1));
   IB_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));

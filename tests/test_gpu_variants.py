@@ -1,0 +1,114 @@
+"""Every kernel variant the launch layer can pick is bit-identical to the oracle.
+
+The runtime chooses between kernel variants by shape and size: for hotspot the
+scalar march, the 16-byte vectorised row kernel and the cp.async.bulk (TMA) plane-march pipeline;
+for FDTD the flat lattice kernels and the x-march kernels. IB_HOTSPOT_KERNEL / IB_FDTD_KERNEL /
+IB_HOTSPOT_RPC / IB_TMA_STAGES / IB_FDTD_PPC force a choice, so each variant is checked here at
+shapes its automatic choice would not reach (ragged tiles, tiny chunks, slabs, binary64).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import cpu as ocpu
+from paper_2501_09398_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def env():
+    saved = {}
+
+    def set_(**kw):
+        for k, v in kw.items():
+            saved.setdefault(k, os.environ.get(k))
+            os.environ[k] = str(v)
+
+    yield set_
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+    wl.release_cached_contexts()
+
+
+HOT_SHAPES = [(64, 48), (33, 1024), (7, 4100), (1, 8), (40, 12, 8), (9, 20, 256), (5, 3, 512),
+              (17, 6, 4), (2, 2, 4)]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("kernel", ["scalar", "vec", "tma"])
+@pytest.mark.parametrize("shape", HOT_SHAPES, ids=["x".join(map(str, s)) for s in HOT_SHAPES])
+def test_hotspot_variant_bitwise(gpu, env, shape, kernel, dtype):
+    env(IB_HOTSPOT_KERNEL=kernel)
+    rng = np.random.default_rng(len(shape) * 1000 + shape[0])
+    k = 0.1 if len(shape) == 3 else 0.2
+    state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, k)
+    npd = np.float32 if dtype == "f32" else np.float64
+    want = ocpu.hotspot(state.temperature, state.power, k, 7, npd)
+    got = wl.run_batched(wl.hotspot_program(), state, 7, 1, dtype=dtype).temperature
+    assert np.array_equal(np.asarray(got, npd), want)
+    got = wl.run_loop(wl.hotspot_program(), state, 7, dtype=dtype, pdl=True).temperature
+    assert np.array_equal(np.asarray(got, npd), want)
+
+
+@pytest.mark.parametrize("rpc,stages", [(1, 3), (2, 3), (3, 4), (5, 8), (64, 4)])
+def test_hotspot_tma_chunking_and_ring_depth(gpu, env, rpc, stages):
+    env(IB_HOTSPOT_KERNEL="tma", IB_HOTSPOT_RPC=rpc, IB_TMA_STAGES=stages)
+    rng = np.random.default_rng(rpc * 31 + stages)
+    for shape in ((23, 16, 256), (29, 40, 8), (31, 2048)):
+        state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
+        want = ocpu.hotspot(state.temperature, state.power, 0.1, 5, np.float32)
+        got = wl.run_batched(wl.hotspot_program(), state, 5, 1, dtype="f32").temperature
+        assert np.array_equal(np.asarray(got, np.float32), want), shape
+
+
+@pytest.mark.parametrize("kernel", ["vec", "tma", "scalar"])
+@pytest.mark.parametrize("slabs", [2, 3, 5])
+def test_hotspot_variants_with_slabs(gpu, env, kernel, slabs):
+    env(IB_HOTSPOT_KERNEL=kernel, IB_HOTSPOT_RPC=3)
+    rng = np.random.default_rng(slabs)
+    for shape in ((30, 12, 8), (41, 64)):
+        state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
+        want = ocpu.hotspot(state.temperature, state.power, 0.1, 6, np.float64)
+        got = wl.run_batched(wl.hotspot_program(), state, 3, 2, devices=[0] * slabs, build="capture")
+        assert np.array_equal(got.temperature, want), shape
+
+
+FDTD_DIMS = [(8, 4, 8), (5, 6, 7), (1, 1, 1), (3, 1, 9), (16, 9, 33), (2, 40, 3)]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("kernel,ppc", [("lean", 0), ("flat", 0), ("march", 0), ("march", 1), ("march", 2),
+                                        ("march", 5)])
+@pytest.mark.parametrize("dims", FDTD_DIMS, ids=["x".join(map(str, d)) for d in FDTD_DIMS])
+def test_fdtd_variant_bitwise(gpu, env, dims, kernel, ppc, dtype):
+    env(IB_FDTD_KERNEL=kernel, IB_FDTD_PPC=ppc)
+    base = wl.fdtd_cavity(*dims)
+    rng = np.random.default_rng(sum(dims) + ppc)
+    state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
+                            base.cell_size, base.time_step)
+    npd = np.float32 if dtype == "f32" else np.float64
+    dt = state.time_step
+    want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
+                     dt / wl.VACUUM_PERMITTIVITY, 4, npd)
+    got = wl.run_batched(wl.fdtd_program(), state, 2, 2, dtype=dtype, pdl=True)
+    for g, w in zip(got.state_arrays(), want):
+        assert np.array_equal(np.asarray(g, npd), w)
+
+
+def test_fdtd_non_unit_cell_size(gpu, env):
+    """d != 1 exercises the division path (skipped exactly when d == 1)."""
+    for kernel in ("lean", "flat", "march"):
+        env(IB_FDTD_KERNEL=kernel)
+        w = wl.te101_cavity(6, 5, 7, cell_size=0.37)
+        dt = w.time_step
+        want = ocpu.fdtd(w.state_arrays(), 0.37, dt / wl.VACUUM_PERMEABILITY,
+                         dt / wl.VACUUM_PERMITTIVITY, 9, np.float64)
+        got = wl.run_loop(wl.fdtd_program(), w, 9)
+        for g, ww in zip(got.state_arrays(), want):
+            assert np.array_equal(g, ww)
