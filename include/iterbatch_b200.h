@@ -58,6 +58,8 @@ extern "C" {
 #define IB_FLAG_NO_UPLOAD 0x4     /* skip cudaGraphUpload (first launch pays the upload) */
 #define IB_FLAG_WHILE 0x8         /* wrap the K-chain in a conditional WHILE node: one cudaGraphLaunch
                                      runs all num_batches batches (device-side loop, no host gap) */
+#define IB_FLAG_MEMINFO 0x10      /* fill ib_times.graph_bytes from cudaMemGetInfo before/after the
+                                     build (the paper's m_base/m_node probe; costs ~ms per call) */
 
 /* Per-call timing record. Host times are steady-clock seconds; gpu_s is CUDA-event time on the
  * context's launch stream (first launch .. end of last kernel). */

@@ -165,7 +165,7 @@ def _cmd_sweep(args) -> int:
     for k in sizes:
         plan = BatchPlan.from_batch_size(total, k)
         g = wl.time_workload_phases(program, state, plan, wl.ExecutionOrder.BATCHED,
-                                    args.repeats, **kw)
+                                    args.repeats, meminfo=True, **kw)
         s = wl.time_workload_phases(program, state, plan, wl.ExecutionOrder.LOOP,
                                     args.repeats, **kw)
         creation.append(MeasurementPoint(k, tuple(g["creation"])))

@@ -1013,7 +1013,8 @@ int ib_graph_build(ib_ctx *c, int64_t batch_size, int build_mode, int flags, ib_
   c->gmode = build_mode;
   ib_times t = {};
   size_t f0 = 0, f1 = 0, tot = 0;
-  IB_CUDA(cudaMemGetInfo(&f0, &tot));
+  const bool meminfo = (flags & IB_FLAG_MEMINFO) != 0;
+  if (meminfo) IB_CUDA(cudaMemGetInfo(&f0, &tot));
   int rc = build_one(c, c->cur, &t);
   if (rc == IB_OK && c->ping_pong() && (batch_size & 1)) rc = build_one(c, c->cur ^ 1, &t);
   if (rc != IB_OK) {
@@ -1022,8 +1023,10 @@ int ib_graph_build(ib_ctx *c, int64_t batch_size, int build_mode, int flags, ib_
     g_err = msg;
     return rc;
   }
-  IB_CUDA(cudaMemGetInfo(&f1, &tot));
-  t.graph_bytes = (int64_t)f0 - (int64_t)f1;
+  if (meminfo) {
+    IB_CUDA(cudaMemGetInfo(&f1, &tot));
+    t.graph_bytes = (int64_t)f0 - (int64_t)f1;
+  }
   if (tm) *tm = t;
   return IB_OK;
 }

@@ -432,11 +432,18 @@ class DeviceSolver:
 
     def build_graph(self, batch_size: int, build: str = "manual", pdl: bool = False,
                     device_launch: bool = False, upload: bool = True,
-                    while_loop: bool = False) -> Times:
+                    while_loop: bool = False, meminfo: bool = False) -> Times:
+        """Unroll batch_size iterations into a graph, instantiate and upload it (T_C).
+
+        ``meminfo`` also records the device memory the instantiated graph(s) took
+        (``Times.graph_bytes``, the paper's memory probe); it costs milliseconds, so timing runs
+        leave it off.
+        """
         if build not in _lib.BUILD:
             raise ValueError(f"build must be one of {sorted(_lib.BUILD)}, got {build!r}")
         flags = ((_lib.FLAG_PDL if pdl else 0) | (_lib.FLAG_DEVICE_LAUNCH if device_launch else 0)
-                 | (0 if upload else _lib.FLAG_NO_UPLOAD) | (_lib.FLAG_WHILE if while_loop else 0))
+                 | (0 if upload else _lib.FLAG_NO_UPLOAD) | (_lib.FLAG_WHILE if while_loop else 0)
+                 | (_lib.FLAG_MEMINFO if meminfo else 0))
         t = _lib.IbTimes()
         _lib.check(_lib.lib().ib_graph_build(self.ctx, int(batch_size), _lib.BUILD[build], flags,
                                              ctypes.byref(t)))
@@ -687,7 +694,7 @@ def time_workload(program, state, plan, order, repeats: int = 10, workers: int |
 
 def time_workload_phases(program, state, plan, order, repeats: int = 10, *, dtype="f64",
                          devices=None, build: str = "manual", pdl: bool = False,
-                         while_loop: bool = False) -> dict:
+                         while_loop: bool = False, meminfo: bool = False) -> dict:
     """Per-repeat samples split into the paper's phases.
 
     Returns {"creation": [T_C...], "execution": [T_E...], "total": [...], "gpu": [device T_E...],
@@ -706,7 +713,8 @@ def time_workload_phases(program, state, plan, order, repeats: int = 10, *, dtyp
             s.upload(state)
         if batched:
             t0 = time.perf_counter()
-            tb = s.build_graph(plan.batch_size, build=build, pdl=pdl, while_loop=while_loop)
+            tb = s.build_graph(plan.batch_size, build=build, pdl=pdl, while_loop=while_loop,
+                               meminfo=meminfo and r == 0)
             te = s.run_graph(plan.num_batches)
             total = time.perf_counter() - t0
             s.destroy_graph()
