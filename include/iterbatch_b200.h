@@ -150,6 +150,40 @@ int ib_host_free(void *ptr);
 uint64_t ib_fnv1a64(const void *data, size_t nbytes, uint64_t h);
 uint64_t ib_fnv1a64_f64(const void *values, size_t n, int dtype, uint64_t h);
 
+/* ---- multi-process slabs (one process per GPU) -------------------------------
+ * A distributed hotspot context owns the axis-0 slab [rows*rank//nranks, rows*(rank+1)//nranks)
+ * of a global grid (dims = GLOBAL dims) on `device`, plus one halo plane per interior face. After
+ * every iteration's stencil kernel the runtime exchanges boundary planes with rank-1 / rank+1 by
+ * NCCL send/recv on the launch stream (libnccl.so.2 is dlopen'ed; graphs are stream-captured, so
+ * the exchange is part of the iteration-batch graph). All ranks call ib_create_dist collectively
+ * with the same 128-byte id from ib_nccl_unique_id on rank 0.
+ * For these contexts ib_upload takes the slab WITH its halo rows, i.e. global rows
+ * [lo - has_top, hi + has_bot) for the temperature and [lo, hi) for the power; ib_download
+ * returns the owned rows [lo, hi). ib_slab_info reports lo, hi, has_top, has_bot. */
+int ib_nccl_unique_id(void *id128);
+int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
+                   const double *scalars, int nscalars, int device, int rank, int nranks,
+                   const void *id128);
+int ib_slab_info(const ib_ctx *ctx, int64_t *lo, int64_t *hi, int *has_top, int *has_bot);
+
+/* ---- real traces (the reference's EventTrace schema, simulate.py:28-36, fileio.py:48) ---------
+ * ib_trace_enable(ctx, capacity > 0) clears and arms tracing for up to `capacity` kernels; 0 disarms.
+ * While armed (single-slab contexts; one traced context per device at a time) every kernel records
+ * its grid's [start, end] from %globaltimer, mapped onto the host steady clock (calibrated at arm
+ * time, about +-5 us), and the runtime logs host events: node added (0), graph instantiated (1),
+ * graph uploaded (2), graph launched (3), baseline kernel launched (7), build started (100).
+ * ib_trace_kernels returns the number of kernels recorded and copies [start_ns, end_ns] pairs;
+ * ib_trace_host_events returns the number of host events and copies (t_ns, kind, batch, kernel). */
+#define IB_EV_NODE_ADDED 0
+#define IB_EV_GRAPH_INSTANTIATED 1
+#define IB_EV_GRAPH_UPLOADED 2
+#define IB_EV_GRAPH_LAUNCHED 3
+#define IB_EV_BASELINE_KERNEL_LAUNCHED 7
+#define IB_EV_BUILD_STARTED 100
+int ib_trace_enable(ib_ctx *ctx, int64_t capacity);
+int64_t ib_trace_kernels(ib_ctx *ctx, int64_t *start_end_ns, int64_t capacity);
+int64_t ib_trace_host_events(ib_ctx *ctx, int64_t *rows4, int64_t capacity);
+
 /* ---- L2 flush helper for benchmark hygiene (writes a buffer larger than L2) ----------------- */
 int ib_flush_l2(ib_ctx *ctx);
 

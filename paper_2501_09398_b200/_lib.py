@@ -75,6 +75,14 @@ PROTOTYPES = [
     ("ib_host_free", _I, [_P]),
     ("ib_fnv1a64", _U64, [_P, _SZ, _U64]),
     ("ib_fnv1a64_f64", _U64, [_P, _SZ, _I, _U64]),
+    ("ib_nccl_unique_id", _I, [_P]),
+    ("ib_create_dist", _I, [ctypes.POINTER(_P), _I, _I, ctypes.POINTER(_I64), _I, ctypes.POINTER(_D), _I,
+                            _I, _I, _I, _P]),
+    ("ib_slab_info", _I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I),
+                          ctypes.POINTER(_I)]),
+    ("ib_trace_enable", _I, [_P, _I64]),
+    ("ib_trace_kernels", _I64, [_P, ctypes.POINTER(_I64), _I64]),
+    ("ib_trace_host_events", _I64, [_P, ctypes.POINTER(_I64), _I64]),
     ("ib_flush_l2", _I, [_P]),
 ]
 

@@ -122,6 +122,13 @@ def build_parser() -> argparse.ArgumentParser:
     sw.add_argument("--repeats", type=int, default=10)
     sw.add_argument("--out", required=True, metavar="DIR")
     sw.set_defaults(func=_cmd_sweep)
+
+    tr = commands.add_parser("trace", help="record real graph/stream timelines in the reference "
+                             "trace schema and write the measured model constants")
+    common(tr)
+    tr.add_argument("--batch-size", type=int, required=True, metavar="S")
+    tr.add_argument("--out", required=True, metavar="DIR")
+    tr.set_defaults(func=_cmd_trace)
     return parser
 
 
@@ -194,6 +201,37 @@ def _cmd_sweep(args) -> int:
     with open(os.path.join(args.out, "summary.json"), "w") as fh:
         json.dump({"workload": args.workload, "size": args.size, "iterations": total,
                    "dtype": args.dtype, "build": args.build, "pdl": args.pdl, "rows": summary}, fh, indent=1)
+    return 0
+
+
+def _cmd_trace(args) -> int:
+    from . import trace as tr
+    from . import workloads as wl
+
+    state = build_workload(args.workload, args.size)
+    plan = BatchPlan.from_batch_size(args.iterations, args.batch_size)
+    os.makedirs(args.out, exist_ok=True)
+    with wl.DeviceSolver(state, args.dtype, devices=args.devices) as s:
+        s.run_batched(plan.batch_size, plan.num_batches, pdl=args.pdl)  # warm-up
+        s.upload(state)
+        g = tr.capture_graph(s, plan.batch_size, plan.num_batches, pdl=args.pdl)
+        s.upload(state)
+        st = tr.capture_stream(s, plan.total_kernel_executions)
+        # memory model m = m_base + m_node * nodes (model.py:130-142): two graph sizes
+        kpi = s.kernels_per_iteration
+        b1 = s.build_graph(plan.batch_size, meminfo=True).graph_bytes
+        s.destroy_graph()
+        b2 = s.build_graph(2 * plan.batch_size, meminfo=True).graph_bytes
+        s.destroy_graph()
+    params = tr.derive_parameters(g, st)
+    n1 = plan.batch_size * kpi
+    m_node = max(0, (b2 - b1) // n1)
+    memory = {"m_base": max(0, b1 - m_node * n1), "m_node": m_node}
+    tr.write_trace_csv(g, os.path.join(args.out, "graph_trace.csv"))
+    tr.write_trace_csv(st, os.path.join(args.out, "stream_trace.csv"))
+    tr.write_params(os.path.join(args.out, "params.txt"), params, memory)
+    print(json.dumps({"workload": args.workload, "size": args.size, "iterations": args.iterations,
+                      "batch_size": args.batch_size, "dtype": args.dtype, **params, **memory}))
     return 0
 
 

@@ -36,6 +36,52 @@ template <> struct rn<double> {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
+// ---- real-trace capture (timelines in the reference's EventTrace schema) --------
+// When a context enables tracing, c_trace points at a TraceBuf and every kernel records its grid's
+// [first CTA start, last CTA end] in %globaltimer ns: thread 0 of each CTA folds its start/end in
+// with atomicMin/atomicMax, and the last CTA to finish appends the pair and resets the
+// accumulators (the next kernel cannot start before this grid completed: stream order or
+// griddepcontrol.wait). Off (nullptr) it costs one uniform constant load and a branch.
+struct TraceBuf {
+  unsigned long long start, end;
+  unsigned int done, seq, cap, pad;
+  unsigned long long rec[2];  // 2*cap entries follow
+};
+__constant__ TraceBuf *c_trace;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct TraceScope {
+  __device__ __forceinline__ TraceScope() {
+    TraceBuf *tb = c_trace;
+    if (tb && threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) atomicMin(&tb->start, gtimer());
+  }
+  __device__ __forceinline__ ~TraceScope() {
+    TraceBuf *tb = c_trace;
+    if (!tb || threadIdx.x != 0 || threadIdx.y != 0 || threadIdx.z != 0) return;
+    atomicMax(&tb->end, gtimer());
+    __threadfence();
+    const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(&tb->done, 1u) == total - 1) {
+      __threadfence();
+      const unsigned int s = tb->seq;
+      if (s < tb->cap) {
+        tb->rec[2 * s] = atomicAdd(&tb->start, 0ull);
+        tb->rec[2 * s + 1] = atomicAdd(&tb->end, 0ull);
+      }
+      tb->seq = s + 1;
+      tb->start = ~0ull;
+      tb->end = 0ull;
+      tb->done = 0u;
+      __threadfence();
+    }
+  }
+};
+
 // ================================================================================================
 // Skeleton: vector scale, in place.  workloads.py:97-105  out = values * c
 //   binary64: v' = v (*) c
@@ -46,6 +92,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __global__ void __launch_bounds__(256) k_vector_f32(float *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
+  TraceScope trace_scope_;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n4 = n >> 2;
   if (i < n4) {
@@ -64,6 +111,7 @@ __global__ void __launch_bounds__(256) k_vector_f32(float *__restrict__ v, int64
 __global__ void __launch_bounds__(256) k_vector_f64(double *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
+  TraceScope trace_scope_;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n2 = n >> 1;
   if (i < n2) {
@@ -105,6 +153,7 @@ __global__ void __launch_bounds__(256)
   const int i0 = blockIdx.y * rows_per_chunk;
   const int i1 = min(rows, i0 + rows_per_chunk);
   pdl_wait();
+  TraceScope trace_scope_;
   if (p >= plane || i0 >= rows) return;
   const int j = D3 ? (int)(p / L) : (int)p;
   const int l = D3 ? (int)(p - (int64_t)j * L) : 0;
@@ -182,6 +231,7 @@ __global__ void __launch_bounds__(256)
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
   const int i = blockIdx.y;
   pdl_wait();
+  TraceScope trace_scope_;
   if (m >= M) return;
   const T *s = src + (int64_t)i * M + m;
   T c[V], up[V], dn[V], ym[V], yp[V], pw[V];
@@ -294,6 +344,7 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   pdl_wait();  // from here on the previous kernel's writes are visible
+  TraceScope trace_scope_;
   auto issue = [&](int t) {
     const int s = t % nstages;
     int q = i0 - 1 + t;
@@ -414,6 +465,7 @@ __global__ void __launch_bounds__(256)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   pdl_wait();
+  TraceScope trace_scope_;
   if (p >= (int64_t)(ny + 1) * pw) return;
   const int j = (int)(p / pw);
   const int k = (int)(p - (int64_t)j * pw);
@@ -452,6 +504,7 @@ __global__ void __launch_bounds__(256)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   pdl_wait();
+  TraceScope trace_scope_;
   if (p >= (int64_t)(ny + 1) * pw) return;
   const int j = (int)(p / pw);
   const int k = (int)(p - (int64_t)j * pw);
@@ -510,6 +563,7 @@ __global__ void __launch_bounds__(256)
   const int i0 = blockIdx.y * planes_per_cta;
   const int i1 = min(nx + 1, i0 + planes_per_cta);
   pdl_wait();
+  TraceScope trace_scope_;
   if (p >= (ny + 1) * pw) return;
   const int j = p / pw;
   const int k = p - j * pw;
@@ -552,6 +606,7 @@ __global__ void __launch_bounds__(256)
   const int i0 = blockIdx.y * planes_per_cta;
   const int i1 = min(nx + 1, i0 + planes_per_cta);
   pdl_wait();
+  TraceScope trace_scope_;
   if (p >= (ny + 1) * pw) return;
   const int j = p / pw;
   const int k = p - j * pw;
@@ -628,6 +683,7 @@ __global__ void __launch_bounds__(256)
   const int j = blockIdx.y * 8 + threadIdx.y;
   const int i = blockIdx.z;
   pdl_wait();
+  TraceScope trace_scope_;
   if (k > nz || j > ny) return;
   const int nz1 = nz + 1, ny1 = ny + 1;
   const int A = (i * ny1 + j) * nz1 + k;
@@ -663,6 +719,7 @@ __global__ void __launch_bounds__(256)
   const int j = blockIdx.y * 8 + threadIdx.y;
   const int i = blockIdx.z;
   pdl_wait();
+  TraceScope trace_scope_;
   if (k > nz || j > ny) return;
   const int nz1 = nz + 1, ny1 = ny + 1;
   const int A = (i * ny1 + j) * nz1 + k;

@@ -12,6 +12,7 @@
 //                                          halo planes pushed by the stencil kernel itself
 // The state lives in HBM for the whole run; the boundary is crossed by ib_upload/ib_download.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -121,6 +122,45 @@ int64_t env_int(const char *name, int64_t dflt) {
   return std::strtoll(v, nullptr, 10);
 }
 
+// ---- NCCL, loaded at run time (no link dependency; the process may already hold torch's copy) --
+struct NcclId { char internal[128]; };
+struct Nccl {
+  bool ok = false;
+  std::string err;
+  int (*GetUniqueId)(NcclId *) = nullptr;
+  int (*CommInitRank)(void **, int, NcclId, int) = nullptr;
+  int (*CommDestroy)(void *) = nullptr;
+  int (*Send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*Recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(int) = nullptr;
+};
+Nccl &nccl() {
+  static Nccl n = [] {
+    Nccl r;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      r.err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+      return r;
+    }
+    r.GetUniqueId = (int (*)(NcclId *))dlsym(h, "ncclGetUniqueId");
+    r.CommInitRank = (int (*)(void **, int, NcclId, int))dlsym(h, "ncclCommInitRank");
+    r.CommDestroy = (int (*)(void *))dlsym(h, "ncclCommDestroy");
+    r.Send = (int (*)(const void *, size_t, int, int, void *, cudaStream_t))dlsym(h, "ncclSend");
+    r.Recv = (int (*)(void *, size_t, int, int, void *, cudaStream_t))dlsym(h, "ncclRecv");
+    r.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
+    r.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+    r.GetErrorString = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
+    r.ok = r.GetUniqueId && r.CommInitRank && r.CommDestroy && r.Send && r.Recv && r.GroupStart &&
+           r.GroupEnd && r.GetErrorString;
+    if (!r.ok) r.err = "libnccl.so.2 lacks a required symbol";
+    return r;
+  }();
+  return n;
+}
+constexpr int kNcclInt8 = 0;  // ncclInt8: halo planes move as raw bytes
+
 }  // namespace
 
 struct ib_ctx {
@@ -146,6 +186,23 @@ struct ib_ctx {
   int *d_counter = nullptr;  // WHILE-mode remaining-batch counter
   void *flush = nullptr;
   size_t flush_bytes = 0;
+  // multi-process slab (ib_create_dist)
+  int rank = 0, nranks = 1;
+  void *comm = nullptr;  // ncclComm_t
+  bool dist() const { return comm != nullptr; }
+  // tracing
+  ib::TraceBuf *d_trace = nullptr;
+  int64_t trace_cap = 0;
+  int64_t gpu_to_host_ns = 0;  // host_ns = gpu_ns + offset
+  struct HostEv { int64_t t, kind, batch, kernel; };
+  std::vector<HostEv> host_ev;
+  bool tracing() const { return d_trace != nullptr; }
+  void ev(int kind, int64_t batch = -1, int64_t kernel = -1) {
+    if (!d_trace) return;
+    const int64_t t = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                          std::chrono::steady_clock::now().time_since_epoch()).count();
+    host_ev.push_back({t, kind, batch, kernel});
+  }
 
   cudaStream_t stream() const { return slabs[0].stream; }
   bool ping_pong() const {
@@ -234,7 +291,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
   const T k = (T)c->scalars[0];
   const T loss = (T)(2.0 * (d3 ? 3 : 2));
   const int P = (int)c->slabs.size();
-  const bool multi = P > 1;
+  const bool multi = P > 1 || c->dist();  // slab buffers carry halo planes
   for (int g = 0; g < P; ++g) {
     Slab &s = c->slabs[g];
     const int rows = s.rows();
@@ -242,11 +299,11 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     const T *src = (const T *)s.buf[parity] + off;
     T *dst = (T *)s.buf[parity ^ 1] + off;
     T *up = nullptr, *dn = nullptr;
-    if (multi && g > 0) {  // my first owned row -> upper neighbour's bottom halo
+    if (P > 1 && g > 0) {  // my first owned row -> upper neighbour's bottom halo
       Slab &n = c->slabs[g - 1];
       up = (T *)n.buf[parity ^ 1] + (int64_t)(n.rows() + 1) * plane;
     }
-    if (multi && g + 1 < P) {  // my last owned row -> lower neighbour's top halo
+    if (P > 1 && g + 1 < P) {  // my last owned row -> lower neighbour's top halo
       Slab &n = c->slabs[g + 1];
       dn = (T *)n.buf[parity ^ 1];
     }
@@ -397,6 +454,31 @@ int launch_one(Launch &L, cudaStream_t s, bool pdl) {
   return IB_OK;
 }
 
+// Halo exchange of a distributed slab after an iteration that wrote buf[parity]:
+// send my first owned plane to rank-1 and receive its last into my top halo; the mirror with
+// rank+1. One NCCL group, on the launch stream (captured into graphs like the kernels).
+int nccl_exchange(ib_ctx *c, int parity, cudaStream_t st) {
+  Nccl &n = nccl();
+  Slab &s = c->slabs[0];
+  const size_t pb = (size_t)(c->plane() * c->esize);
+  char *b = (char *)s.buf[parity];
+  auto chk = [&](int r, const char *what) {
+    if (r != 0) return fail(IB_ECUDA, std::string(what) + ": " + n.GetErrorString(r));
+    return IB_OK;
+  };
+  IB_TRY(chk(n.GroupStart(), "ncclGroupStart"));
+  if (s.has_top) {
+    IB_TRY(chk(n.Send(b + pb, pb, kNcclInt8, c->rank - 1, c->comm, st), "ncclSend(up)"));
+    IB_TRY(chk(n.Recv(b, pb, kNcclInt8, c->rank - 1, c->comm, st), "ncclRecv(up)"));
+  }
+  if (s.has_bot) {
+    IB_TRY(chk(n.Send(b + (size_t)s.rows() * pb, pb, kNcclInt8, c->rank + 1, c->comm, st), "ncclSend(down)"));
+    IB_TRY(chk(n.Recv(b + (size_t)(s.rows() + 1) * pb, pb, kNcclInt8, c->rank + 1, c->comm, st), "ncclRecv(down)"));
+  }
+  IB_TRY(chk(n.GroupEnd(), "ncclGroupEnd"));
+  return IB_OK;
+}
+
 // Enqueue `iters` iterations starting at `parity` onto the slab streams (also used under stream
 // capture). Multi-slab: kernel(g,t) waits for kernel(g+-1,t-1) — RAW on the halo it reads and
 // WAR on the halo it writes — through double-buffered events.
@@ -423,9 +505,15 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
       }
       // PDL only chains kernels on the same stream; the very first launch has no predecessor.
       const bool use_pdl = pdl && P == 1 && (t > 0 || q > 0);
+      c->ev(single_stream ? IB_EV_NODE_ADDED : IB_EV_BASELINE_KERNEL_LAUNCHED, single_stream ? -1 : t,
+            single_stream ? nk : (int64_t)q);
       IB_TRY(launch_one(L, st, use_pdl));
       if (P > 1) IB_CUDA(cudaEventRecord(s.ev[t & 1], st));
       ++nk;
+    }
+    if (c->dist()) {  // boundary planes of this iteration's output <-> neighbouring ranks
+      cudaStream_t st = single_stream ? single_stream : c->slabs[0].stream;
+      IB_TRY(nccl_exchange(c, par ^ 1, st));
     }
     if (c->ping_pong()) par ^= 1;
   }
@@ -500,6 +588,7 @@ int build_manual_chain(ib_ctx *c, cudaGraph_t graph, int64_t K, int parity, bool
         IB_CUDA(cudaGraphAddDependencies_v2(graph, &prev, &node, &ed, 1));
       }
       prev = node;
+      c->ev(IB_EV_NODE_ADDED, -1, *nodes);
       ++*nodes;
     }
     if (c->ping_pong()) par ^= 1;
@@ -526,9 +615,10 @@ int build_one(ib_ctx *c, int parity, ib_times *tm) {
   const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
   const int P = (int)c->slabs.size();
   int64_t nodes = 0;
+  c->ev(IB_EV_BUILD_STARTED);
   auto a = clk::now();
   cudaGraph_t g = nullptr;
-  if (c->gmode == IB_BUILD_MANUAL && P == 1) {
+  if (c->gmode == IB_BUILD_MANUAL && P == 1 && !c->dist()) {
     IB_CUDA(cudaGraphCreate(&g, 0));
     cudaGraph_t body = g;
     if (wh) {
@@ -589,11 +679,13 @@ int build_one(ib_ctx *c, int parity, ib_times *tm) {
     return fail(IB_ECUDA, std::string("cudaGraphInstantiateWithFlags: ") + cudaGetErrorString(ie));
   }
   auto d = clk::now();
+  c->ev(IB_EV_GRAPH_INSTANTIATED);
   if (!(c->gflags & IB_FLAG_NO_UPLOAD)) {
     IB_CUDA(cudaGraphUpload(ex, c->stream()));
     IB_CUDA(cudaStreamSynchronize(c->stream()));
   }
   auto e2 = clk::now();
+  c->ev(IB_EV_GRAPH_UPLOADED);
   c->graph[parity] = g;
   c->exec[parity] = ex;
   if (tm) {
@@ -646,6 +738,10 @@ void ib_destroy(ib_ctx *c) {
   DeviceGuard guard;
   if (!c->slabs.empty()) cudaSetDevice(c->slabs[0].device);
   free_graphs(c);
+  if (c->comm) {
+    nccl().CommDestroy(c->comm);
+    c->comm = nullptr;
+  }
   for (Slab &s : c->slabs) {
     cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);
@@ -661,6 +757,11 @@ void ib_destroy(ib_ctx *c) {
   for (int f = 0; f < 6; ++f)
     if (c->field[f]) cudaFree(c->field[f]);
   if (c->d_counter) cudaFree(c->d_counter);
+  if (c->d_trace) {
+    ib::TraceBuf *none = nullptr;
+    cudaMemcpyToSymbol(ib::c_trace, &none, sizeof(none));
+    cudaFree(c->d_trace);
+  }
   if (c->flush) cudaFree(c->flush);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
@@ -675,13 +776,17 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   const int64_t rows = hot ? c->dims[0] : 1;
   if (P > rows) return fail(IB_EINVAL, "more slabs than rows along axis 0");
   c->slabs.resize(P);
+  const bool dist = c->nranks > 1;
+  if (dist && (P != 1 || !hot)) return fail(IB_EINVAL, "distributed contexts are single-slab hotspot grids");
+  if (dist && c->nranks > rows) return fail(IB_EINVAL, "more ranks than rows along axis 0");
   for (int g = 0; g < P; ++g) {
     Slab &s = c->slabs[g];
     s.device = devices[g];
-    s.row_lo = (int)(rows * g / P);  // workloads.py:65 bounds formula
-    s.row_hi = (int)(rows * (g + 1) / P);
-    s.has_top = g > 0;
-    s.has_bot = g + 1 < P;
+    const int64_t G = dist ? c->rank : g, NP = dist ? c->nranks : P;
+    s.row_lo = (int)(rows * G / NP);  // workloads.py:65 bounds formula
+    s.row_hi = (int)(rows * (G + 1) / NP);
+    s.has_top = G > 0;
+    s.has_bot = G + 1 < NP;
     IB_CUDA(cudaSetDevice(s.device));
     IB_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     for (int p = 0; p < 2; ++p) IB_CUDA(cudaEventCreateWithFlags(&s.ev[p], cudaEventDisableTiming));
@@ -712,7 +817,7 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
     const int64_t plane = c->plane();
     for (Slab &s : c->slabs) {
       IB_CUDA(cudaSetDevice(s.device));
-      const int64_t planes = s.rows() + (P > 1 ? 2 : 0);
+      const int64_t planes = s.rows() + (P > 1 || dist ? 2 : 0);
       for (int p = 0; p < 2; ++p) {
         IB_CUDA(cudaMalloc(&s.buf[p], (size_t)(planes * plane * es)));
         IB_CUDA(cudaMemset(s.buf[p], 0, (size_t)(planes * plane * es)));
@@ -732,8 +837,9 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   return IB_OK;
 }
 
-int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
-              const double *scalars, int nscalars, const int *devices, int ndevices) {
+static int create_common(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
+                         const double *scalars, int nscalars, const int *devices, int ndevices,
+                         int rank, int nranks, const void *id128) {
   if (!out) return fail(IB_EINVAL, "out is null");
   *out = nullptr;
   if (solver < IB_SOLVER_VECTOR || solver > IB_SOLVER_FDTD) return fail(IB_EINVAL, "unknown solver");
@@ -774,6 +880,8 @@ int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndim
   c->ndims = ndims;
   for (int i = 0; i < ndims; ++i) c->dims[i] = dims[i];
   for (int i = 0; i < nscalars; ++i) c->scalars[i] = scalars[i];
+  c->rank = rank;
+  c->nranks = nranks;
   if (solver == IB_SOLVER_FDTD && !(scalars[0] > 0.0)) {
     delete c;
     return fail(IB_EINVAL, "cell_size must be positive");
@@ -803,6 +911,21 @@ int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndim
     }
   }
   int rc = create_impl(c, devs.data(), (int)devs.size());
+  if (rc == IB_OK && nranks > 1) {
+    Nccl &n = nccl();
+    if (!n.ok) {
+      rc = fail(IB_ECUDA, n.err);
+    } else {
+      NcclId id;
+      std::memcpy(id.internal, id128, sizeof(id.internal));
+      cudaSetDevice(c->slabs[0].device);
+      const int r = n.CommInitRank(&c->comm, nranks, id, rank);
+      if (r != 0) {
+        c->comm = nullptr;
+        rc = fail(IB_ECUDA, std::string("ncclCommInitRank: ") + n.GetErrorString(r));
+      }
+    }
+  }
   if (rc != IB_OK) {
     std::string msg = g_err;
     ib_destroy(c);
@@ -810,6 +933,44 @@ int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndim
     return rc;
   }
   *out = c;
+  return IB_OK;
+}
+
+int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
+              const double *scalars, int nscalars, const int *devices, int ndevices) {
+  return create_common(out, solver, dtype, dims, ndims, scalars, nscalars, devices, ndevices, 0, 1,
+                       nullptr);
+}
+
+int ib_nccl_unique_id(void *id128) {
+  if (!id128) return fail(IB_EINVAL, "id buffer is null");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(IB_ECUDA, n.err);
+  NcclId id;
+  const int r = n.GetUniqueId(&id);
+  if (r != 0) return fail(IB_ECUDA, std::string("ncclGetUniqueId: ") + n.GetErrorString(r));
+  std::memcpy(id128, id.internal, sizeof(id.internal));
+  return IB_OK;
+}
+
+int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
+                   const double *scalars, int nscalars, int device, int rank, int nranks,
+                   const void *id128) {
+  if (solver != IB_SOLVER_HOTSPOT2D && solver != IB_SOLVER_HOTSPOT3D)
+    return fail(IB_EINVAL, "distributed contexts are defined for hotspot grids");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(IB_EINVAL, "bad rank / nranks");
+  if (nranks > 1 && !id128) return fail(IB_EINVAL, "nranks > 1 needs the NCCL unique id");
+  return create_common(out, solver, dtype, dims, ndims, scalars, nscalars, &device, 1, rank, nranks,
+                       id128);
+}
+
+int ib_slab_info(const ib_ctx *c, int64_t *lo, int64_t *hi, int *has_top, int *has_bot) {
+  IB_TRY(check_ctx(c));
+  const Slab &s = c->slabs[0];
+  if (lo) *lo = c->ping_pong() ? s.row_lo : 0;
+  if (hi) *hi = c->ping_pong() ? s.row_hi : c->dims[0];
+  if (has_top) *has_top = c->nranks > 1 && s.has_top;
+  if (has_bot) *has_bot = c->nranks > 1 && s.has_bot;
   return IB_OK;
 }
 
@@ -851,6 +1012,24 @@ static int hotspot_copy(ib_ctx *c, int field, void *host, size_t bytes, bool up)
   const int64_t pb = plane * c->esize;
   const int P = (int)c->slabs.size();
   char *h = (char *)host;
+  if (c->nranks > 1) {  // local window: [lo - top, hi + bot) up, [lo, hi) down (see header)
+    Slab &s = c->slabs[0];
+    IB_CUDA(cudaSetDevice(s.device));
+    if (field == 1) {
+      IB_CUDA(cudaMemcpyAsync(up ? s.power : host, up ? host : s.power, (size_t)(s.rows() * pb),
+                              up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s.stream));
+    } else if (up) {
+      char *dev = (char *)s.buf[c->cur] + (s.has_top ? 0 : pb);
+      const size_t nb = (size_t)((s.rows() + s.has_top + s.has_bot) * pb);
+      IB_CUDA(cudaMemcpyAsync(dev, h, nb, cudaMemcpyHostToDevice, s.stream));
+    } else {
+      IB_CUDA(cudaMemcpyAsync(h, (char *)s.buf[c->cur] + pb, (size_t)(s.rows() * pb),
+                              cudaMemcpyDeviceToHost, s.stream));
+    }
+    IB_CUDA(cudaStreamSynchronize(s.stream));
+    (void)bytes;
+    return IB_OK;
+  }
   for (int g = 0; g < P; ++g) {
     Slab &s = c->slabs[g];
     IB_CUDA(cudaSetDevice(s.device));
@@ -881,7 +1060,12 @@ static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
   IB_TRY(check_ctx(c));
   if (field < 0 || field >= c->nfields) return fail(IB_EINVAL, "field index out of range");
   if (!host) return fail(IB_EINVAL, "host pointer is null");
-  const int64_t want = ib_field_bytes(c, field);
+  int64_t want = ib_field_bytes(c, field);
+  if (c->nranks > 1) {
+    const Slab &s = c->slabs[0];
+    const int64_t pb = c->plane() * c->esize;
+    want = (field == 0 && up) ? (s.rows() + s.has_top + s.has_bot) * pb : s.rows() * pb;
+  }
   if ((int64_t)bytes != want)
     return fail(IB_EINVAL, "field " + std::to_string(field) + " holds " + std::to_string(want) +
                                " bytes, got " + std::to_string(bytes));
@@ -1052,11 +1236,13 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
         return fail(IB_EINVAL, "IB_FLAG_WHILE with an odd batch_size needs num_batches <= 1 (ping-pong parity)");
       int nb = (int)num_batches;
       IB_CUDA(cudaMemcpyAsync(c->d_counter, &nb, sizeof(int), cudaMemcpyHostToDevice, c->stream()));
+      c->ev(IB_EV_GRAPH_LAUNCHED, 0);
       IB_CUDA(cudaGraphLaunch(c->exec[c->cur], c->stream()));
       t.launches = 1;
       if (c->ping_pong() && (c->K & 1)) c->cur ^= 1;
     } else {
       for (int64_t b = 0; b < num_batches; ++b) {
+        c->ev(IB_EV_GRAPH_LAUNCHED, b);
         IB_CUDA(cudaGraphLaunch(c->exec[c->cur], c->stream()));
         if (c->ping_pong() && (c->K & 1)) c->cur ^= 1;
       }
@@ -1142,6 +1328,86 @@ uint64_t ib_fnv1a64_f64(const void *values, size_t n, int dtype, uint64_t h) {
     }
   }
   return h;
+}
+
+__global__ void k_clock(unsigned long long *out) { *out = ib::gtimer(); }
+
+int ib_trace_enable(ib_ctx *c, int64_t capacity) {
+  IB_TRY(check_ctx(c));
+  if (capacity < 0) return fail(IB_EINVAL, "capacity must be >= 0");
+  if (capacity > 0 && c->slabs.size() > 1) return fail(IB_EINVAL, "tracing needs a single-slab context");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_TRY(sync_all(c));
+  ib::TraceBuf *none = nullptr;
+  IB_CUDA(cudaMemcpyToSymbol(ib::c_trace, &none, sizeof(none)));
+  if (c->d_trace) cudaFree(c->d_trace);
+  c->d_trace = nullptr;
+  c->trace_cap = 0;
+  c->host_ev.clear();
+  if (capacity == 0) return IB_OK;
+  const size_t bytes = sizeof(ib::TraceBuf) + (size_t)capacity * 2 * sizeof(unsigned long long);
+  IB_CUDA(cudaMalloc(&c->d_trace, bytes));
+  ib::TraceBuf init = {};
+  init.start = ~0ull;
+  init.cap = (unsigned)std::min<int64_t>(capacity, 0x7fffffff);
+  IB_CUDA(cudaMemcpy(c->d_trace, &init, sizeof(init), cudaMemcpyHostToDevice));
+  // map %globaltimer onto the host steady clock: the narrowest of 16 launch round trips
+  unsigned long long *d_t = nullptr, g = 0;
+  IB_CUDA(cudaMalloc(&d_t, sizeof(*d_t)));
+  int64_t best_w = INT64_MAX;
+  for (int r = 0; r < 16; ++r) {
+    const int64_t h0 = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                           clk::now().time_since_epoch()).count();
+    k_clock<<<1, 1, 0, c->stream()>>>(d_t);
+    cudaError_t e = cudaStreamSynchronize(c->stream());
+    const int64_t h1 = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                           clk::now().time_since_epoch()).count();
+    if (e != cudaSuccess) {
+      cudaFree(d_t);
+      IB_CUDA(e);
+    }
+    IB_CUDA(cudaMemcpy(&g, d_t, sizeof(g), cudaMemcpyDeviceToHost));
+    if (h1 - h0 < best_w) {
+      best_w = h1 - h0;
+      c->gpu_to_host_ns = (h0 + h1) / 2 - (int64_t)g;
+    }
+  }
+  cudaFree(d_t);
+  c->trace_cap = capacity;
+  IB_CUDA(cudaMemcpyToSymbol(ib::c_trace, &c->d_trace, sizeof(c->d_trace)));
+  return IB_OK;
+}
+
+int64_t ib_trace_kernels(ib_ctx *c, int64_t *out, int64_t capacity) {
+  if (!c || !c->d_trace) return fail(IB_ESTATE, "tracing is not enabled");
+  DeviceGuard guard;
+  cudaSetDevice(c->slabs[0].device);
+  if (sync_all(c) != IB_OK) return IB_ECUDA;
+  ib::TraceBuf hdr;
+  if (cudaMemcpy(&hdr, c->d_trace, sizeof(hdr), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(IB_ECUDA, "trace header copy failed");
+  const int64_t n = std::min<int64_t>(std::min<int64_t>(hdr.seq, c->trace_cap), capacity);
+  if (out && n > 0) {
+    std::vector<unsigned long long> buf((size_t)n * 2);
+    if (cudaMemcpy(buf.data(), c->d_trace->rec, buf.size() * sizeof(unsigned long long),
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail(IB_ECUDA, "trace record copy failed");
+    for (int64_t i = 0; i < 2 * n; ++i) out[i] = (int64_t)buf[(size_t)i] + c->gpu_to_host_ns;
+  }
+  return (int64_t)hdr.seq;
+}
+
+int64_t ib_trace_host_events(ib_ctx *c, int64_t *rows, int64_t capacity) {
+  if (!c || !c->d_trace) return fail(IB_ESTATE, "tracing is not enabled");
+  const int64_t n = (int64_t)c->host_ev.size();
+  for (int64_t i = 0; rows && i < std::min(n, capacity); ++i) {
+    rows[4 * i] = c->host_ev[(size_t)i].t;
+    rows[4 * i + 1] = c->host_ev[(size_t)i].kind;
+    rows[4 * i + 2] = c->host_ev[(size_t)i].batch;
+    rows[4 * i + 3] = c->host_ev[(size_t)i].kernel;
+  }
+  return n;
 }
 
 int ib_flush_l2(ib_ctx *c) {

@@ -1,0 +1,135 @@
+"""One process per GPU: axis-0 slabs of a hotspot grid, halo planes exchanged by NCCL in-graph.
+
+SURVEY.md §8e: the large Hotspot3D grid (2048x2048x256) is partitioned along axis 0 with the
+reference's row-slab bounds ``rows*g//P`` (workloads.py:60-69). Rank g owns rows [lo, hi) and one
+halo plane per interior face. After every iteration's stencil kernel the runtime sends its first
+owned plane to rank g-1 and its last to rank g+1 and receives theirs into its halos — one NCCL
+group on the launch stream, captured into the iteration-batch graph together with the kernels
+(``ib_create_dist`` in include/iterbatch_b200.h). The exchange plan is restated in pure Python
+(``exchange_plan``) so the CPU tests can run the same protocol over gloo against the oracle.
+
+Launch with torchrun (RANK / WORLD_SIZE / LOCAL_RANK); ``torch.distributed`` only carries the
+128-byte NCCL id and the final gather — the data path is the runtime's own NCCL communicator.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .workloads import DeviceSolver, Times, _dims_scalars, _kind_of_state, _norm_dtype, _NP_DTYPE
+
+__all__ = ["slab_bounds", "halo_window", "exchange_plan", "unique_id", "DistributedSolver"]
+
+
+def slab_bounds(rows: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [lo, hi) of rank's slab — the reference's bounds formula (workloads.py:65)."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside [0, {world})")
+    if world > rows:
+        raise ValueError("more ranks than rows along axis 0")
+    return rows * rank // world, rows * (rank + 1) // world
+
+
+def halo_window(rows: int, world: int, rank: int) -> tuple[int, int]:
+    """Global rows a rank uploads: its slab plus one halo row per interior face."""
+    lo, hi = slab_bounds(rows, world, rank)
+    return lo - (1 if rank > 0 else 0), hi + (1 if rank < world - 1 else 0)
+
+
+def exchange_plan(rows: int, world: int, rank: int) -> list[tuple[str, int, int, int]]:
+    """(op, peer, local_row) of one iteration's halo exchange, in the runtime's order.
+
+    local_row indexes the rank's slab buffer of (hi - lo + 2) planes: 0 = top halo,
+    1..n = owned rows, n+1 = bottom halo (runtime.cu: nccl_exchange).
+    """
+    lo, hi = slab_bounds(rows, world, rank)
+    n = hi - lo
+    plan = []
+    if rank > 0:
+        plan += [("send", rank - 1, 1), ("recv", rank - 1, 0)]
+    if rank < world - 1:
+        plan += [("send", rank + 1, n), ("recv", rank + 1, n + 1)]
+    return plan
+
+
+def unique_id() -> bytes:
+    """A fresh NCCL unique id (call on rank 0, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(_lib.lib().ib_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+class DistributedSolver(DeviceSolver):
+    """This rank's slab of a global hotspot grid, resident on one GPU.
+
+    ``state`` is the GLOBAL HotspotWorkload (each rank only uploads its window). Graph builds
+    are stream-captured (the NCCL group is part of every iteration).
+    """
+
+    def __init__(self, state, dtype, rank: int, world: int, device: int, uid: bytes | None,
+                 upload: bool = True):
+        kind = _kind_of_state(state)
+        if kind not in ("hotspot2d", "hotspot3d"):
+            raise ValueError("distributed execution is defined for hotspot grids")
+        self.kind = kind
+        self.dtype = _norm_dtype(dtype)
+        self.np_dtype = _NP_DTYPE[self.dtype]
+        self.dims, self.scalars = _dims_scalars(kind, state)
+        self.devices = (device,)
+        self.rank, self.world = rank, world
+        self.rows = self.dims[0]
+        self.lo, self.hi = slab_bounds(self.rows, world, rank)
+        self.wlo, self.whi = halo_window(self.rows, world, rank)
+        L = _lib.lib()
+        ctx = ctypes.c_void_p()
+        dims = (ctypes.c_int64 * len(self.dims))(*self.dims)
+        sc = (ctypes.c_double * len(self.scalars))(*self.scalars)
+        idp = None
+        if world > 1:
+            if uid is None or len(uid) != 128:
+                raise ValueError("world > 1 needs the 128-byte NCCL unique id from rank 0")
+            self._uid = ctypes.create_string_buffer(uid, 128)
+            idp = ctypes.cast(self._uid, ctypes.c_void_p)
+        _lib.check(L.ib_create_dist(ctypes.byref(ctx), _lib.SOLVER[kind], _lib.DTYPE[self.dtype], dims,
+                                    len(self.dims), sc, len(self.scalars), device, rank, world, idp))
+        self._ctx = ctx
+        self.nfields = 2
+        plane = tuple(self.dims[1:])
+        self.shapes = [(self.hi - self.lo,) + plane, (self.hi - self.lo,) + plane]
+        self.batch_size = 0
+        if upload:
+            self.upload(state)
+
+    def host_arrays(self, state):
+        t = np.ascontiguousarray(state.temperature[self.wlo:self.whi], dtype=self.np_dtype)
+        p = np.ascontiguousarray(state.power[self.lo:self.hi], dtype=self.np_dtype)
+        return [t, p]
+
+    def upload(self, state, fields=None) -> None:
+        arrs = state if isinstance(state, (list, tuple)) else self.host_arrays(state)
+        L = _lib.lib()
+        for f, a in enumerate(arrs):
+            if fields is not None and f not in fields:
+                continue
+            a = np.ascontiguousarray(a, dtype=self.np_dtype)
+            _lib.check(L.ib_upload(self.ctx, f, a.ctypes.data_as(ctypes.c_void_p), a.nbytes))
+
+    def build_graph(self, batch_size: int, build: str = "capture", pdl: bool = False,
+                    device_launch: bool = False, upload: bool = True,
+                    while_loop: bool = False, meminfo: bool = False) -> Times:
+        return super().build_graph(batch_size, "capture", pdl, False, upload, False, meminfo)
+
+    def run_batched(self, batch_size: int, num_batches: int, build: str = "capture",
+                    pdl: bool = False, while_loop: bool = False) -> Times:
+        return super().run_batched(batch_size, num_batches, "capture", pdl, False)
+
+    def local_temperature(self) -> np.ndarray:
+        """This rank's owned rows [lo, hi) of the current temperature."""
+        return self.download_field(0)
+
+    @property
+    def iteration_bytes(self) -> int:
+        return 3 * int(np.prod(self.shapes[0])) * np.dtype(self.np_dtype).itemsize

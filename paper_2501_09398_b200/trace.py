@@ -1,0 +1,182 @@
+"""Real B200 timelines in the reference's EventTrace schema, and the timing parameters they imply.
+
+The reference only *simulates* the Fig. 1 timelines (pkg/src/iterbatch/simulate.py:28-125) and
+reads measured platform constants from a ``key = value`` params file (fileio.py:34-45,70-125).
+This module records the real thing:
+
+* ``capture_graph`` / ``capture_stream`` arm the runtime's trace (``ib_trace_enable``): every
+  kernel's grid [start, end] from %globaltimer, mapped onto the host steady clock, plus the host
+  events of the build and launch calls;
+* ``write_trace_csv`` writes them in the reference trace-CSV schema (``# schema=1``,
+  ``timestamp,kind,batch_index,kernel_index``, 9-decimal seconds, fileio.py:48,193-205), with the
+  clock starting at zero at the build start as the simulator's does; ``iterbatch``'s
+  ``parse_trace_csv`` / ``trace_summary`` read it unchanged;
+* ``derive_parameters`` reduces a graph trace and a stream trace to the model's constants
+  t_k, t_i, t_a, t_l, t_b (model.py:48-74), k_c, b_c from the build events, and
+  ``write_params`` writes the params file ``iterbatch optimize`` consumes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import statistics
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+# reference EventKind values (simulate.py:28-36), indexed by the runtime's IB_EV_* codes
+KIND = {
+    0: "node_added",
+    1: "graph_instantiated",
+    2: "graph_uploaded",
+    3: "graph_launched",
+    4: "kernel_started",
+    5: "kernel_ended",
+    6: "batch_gap_started",
+    7: "baseline_kernel_launched",
+}
+BUILD_STARTED = 100
+TRACE_HEADER = "timestamp,kind,batch_index,kernel_index"
+
+
+@dataclass
+class RealTrace:
+    """Events as (seconds since the build/run start, kind, batch_index | None, kernel_index | None)."""
+
+    mode: str  # "graph" | "baseline"
+    batch_size: int  # nodes per batch (kernels per graph launch); 1 for baseline
+    num_batches: int
+    events: list
+    kernels: np.ndarray  # (n, 2) kernel [start, end] seconds on the same clock
+
+
+def _arm(solver, capacity: int) -> None:
+    _lib.check(_lib.lib().ib_trace_enable(solver.ctx, int(capacity)))
+
+
+def _collect(solver, capacity: int):
+    L = _lib.lib()
+    buf = np.zeros(2 * capacity, dtype=np.int64)
+    n = L.ib_trace_kernels(solver.ctx, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), capacity)
+    if n < 0:
+        _lib.check(int(n))
+    kern = buf[: 2 * min(n, capacity)].reshape(-1, 2)
+    m = L.ib_trace_host_events(solver.ctx, None, 0)
+    rows = np.zeros(4 * max(m, 1), dtype=np.int64)
+    L.ib_trace_host_events(solver.ctx, rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), m)
+    _arm(solver, 0)
+    return kern, rows[: 4 * m].reshape(-1, 4), int(n)
+
+
+def capture_graph(solver, batch_size: int, num_batches: int, pdl: bool = False) -> RealTrace:
+    """Build a batch_size-iteration graph and replay it num_batches times, traced."""
+    kpi = solver.kernels_per_iteration
+    cap = batch_size * num_batches * kpi
+    _arm(solver, cap)
+    solver.build_graph(batch_size, pdl=pdl)
+    solver.run_graph(num_batches)
+    solver.destroy_graph()
+    kern, host, n = _collect(solver, cap)
+    if n != cap:
+        raise RuntimeError(f"trace recorded {n} kernels, expected {cap}")
+    return _assemble("graph", batch_size * kpi, num_batches, kern, host)
+
+
+def capture_stream(solver, iterations: int, pdl: bool = False) -> RealTrace:
+    """Listing 1 (one launch per kernel), traced; each kernel is its own 'batch'."""
+    kpi = solver.kernels_per_iteration
+    cap = iterations * kpi
+    _arm(solver, cap)
+    solver.run_stream(iterations, pdl=pdl)
+    kern, host, n = _collect(solver, cap)
+    if n != cap:
+        raise RuntimeError(f"trace recorded {n} kernels, expected {cap}")
+    return _assemble("baseline", 1, cap, kern, host)
+
+
+def _assemble(mode, size, num, kern, host) -> RealTrace:
+    starts = [r for r in host if r[1] == BUILD_STARTED]
+    t0 = int(starts[0][0]) if starts else int(min(host[0][0] if len(host) else kern[0, 0], kern[0, 0]))
+    ev = []
+    launch_i = 0
+    for t, kind, batch, kernel in host:
+        if kind == BUILD_STARTED:
+            continue
+        if kind == 7:  # baseline launches: one per kernel, indexed as batches of size 1
+            ev.append(((t - t0) * 1e-9, KIND[7], launch_i, 0))
+            launch_i += 1
+            continue
+        if kind == 0:  # an odd-K hotspot graph has a second (swapped-parity) executable
+            kernel = kernel % size
+        ev.append(((t - t0) * 1e-9, KIND[int(kind)], None if batch < 0 else int(batch),
+                   None if kernel < 0 else int(kernel)))
+    ks = (kern - t0) * 1e-9
+    for idx, (a, b) in enumerate(ks):
+        bi, ki = divmod(idx, size)
+        if mode == "graph" and ki == 0 and bi > 0:
+            ev.append((ks[idx - 1, 1], KIND[6], bi, None))
+        ev.append((a, KIND[4], bi, ki))
+        ev.append((b, KIND[5], bi, ki))
+    order = {k: i for i, k in enumerate(KIND.values())}
+    ev.sort(key=lambda e: (e[0], order[e[1]]))
+    return RealTrace(mode, size, num, ev, ks)
+
+
+def write_trace_csv(trace: RealTrace, path) -> None:
+    with open(path, "w") as fh:
+        fh.write("# schema=1\n")
+        fh.write(TRACE_HEADER + "\n")
+        for t, kind, batch, kernel in trace.events:
+            b = "" if batch is None else str(batch)
+            k = "" if kernel is None else str(kernel)
+            fh.write(f"{max(t, 0.0):.9f},{kind},{b},{k}\n")
+
+
+def derive_parameters(graph: RealTrace, stream: RealTrace) -> dict:
+    """The model's platform constants (model.py:48-74) measured from real traces.
+
+    t_k kernel duration; t_i gap between consecutive kernels inside a graph; t_a gap between the
+    last kernel of a graph and the first of the next; t_l first launch call -> first kernel start;
+    t_b kernel-to-kernel gap of the plain launch loop; k_c / b_c per-node and fixed build cost.
+    """
+    g = graph.kernels
+    size = graph.batch_size
+    dur = g[:, 1] - g[:, 0]
+    gaps = g[1:, 0] - g[:-1, 1]
+    idx = np.arange(1, len(g))
+    intra = gaps[(idx % size) != 0]
+    inter = gaps[(idx % size) == 0]
+    s = stream.kernels
+    sgaps = s[1:, 0] - s[:-1, 1]
+    launches = [e[0] for e in graph.events if e[1] == "graph_launched"]
+    nodes = sorted(e[0] for e in graph.events if e[1] == "node_added")
+    inst = [e[0] for e in graph.events if e[1] == "graph_instantiated"]
+    upl = [e[0] for e in graph.events if e[1] == "graph_uploaded"]
+    k_c = (nodes[-1] - nodes[0]) / max(1, len(nodes) - 1) if len(nodes) > 1 else 0.0
+    b_c = (upl[-1] - nodes[-1]) if (upl and nodes) else 0.0
+    med = lambda a: float(statistics.median(a)) if len(a) else 0.0  # noqa: E731
+    return {
+        "t_k": med(dur),
+        "t_i": med(intra) if len(intra) else 0.0,
+        "t_a": med(inter) if len(inter) else 0.0,
+        "t_l": float(g[0, 0] - launches[0]) if launches else 0.0,
+        "t_b": med(sgaps),
+        "k_c": float(k_c),
+        "b_c": float(max(b_c, 0.0)),
+        "kernels_graph": int(len(g)),
+        "kernels_stream": int(len(s)),
+        "instantiate_s": float(inst[-1] - nodes[-1]) if (inst and nodes) else 0.0,
+    }
+
+
+def write_params(path, params: dict, memory: dict | None = None) -> None:
+    """The reference's params file (fileio.py:34-45): t_k t_i t_a t_l t_b k_c b_c [m_base m_node]."""
+    with open(path, "w") as fh:
+        fh.write("# schema=1\n# measured on B200 by paper_2501_09398_b200.trace\n")
+        for key in ("t_k", "t_i", "t_a", "t_l", "t_b", "k_c", "b_c"):
+            fh.write(f"{key} = {max(params[key], 0.0):.6e}\n")
+        if memory:
+            fh.write(f"m_base = {int(memory['m_base'])}\n")
+            fh.write(f"m_node = {int(memory['m_node'])}\n")

@@ -1,0 +1,87 @@
+"""Multi-process slabs on GPUs (ib_create_dist). World 1 runs everywhere; the NCCL halo path needs
+>= 2 GPUs (one process per GPU, like torchrun) and is skipped on a single-GPU box."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2501_09398_b200 import _lib
+from paper_2501_09398_b200 import workloads as wl
+from paper_2501_09398_b200.distributed import DistributedSolver, unique_id
+
+pytestmark = pytest.mark.gpu
+
+
+def _state(shape, seed=3):
+    rng = np.random.default_rng(seed)
+    return wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_world_one_equals_device_solver(gpu, dtype):
+    st = _state((24, 16, 8))
+    ref = wl.run_batched(wl.hotspot_program(), st, 5, 2, dtype=dtype).temperature
+    d = DistributedSolver(st, dtype, rank=0, world=1, device=0, uid=None)
+    d.run_batched(5, 2)
+    assert np.array_equal(d.local_temperature().astype(np.float64), ref)
+    d.close()
+
+
+def test_nccl_is_loadable(gpu):
+    uid = unique_id()
+    assert len(uid) == 128 and any(uid)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _rank_main(rank, world, port, shape, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        obj = [unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        st = _state(shape)
+        d = DistributedSolver(st, "f32", rank=rank, world=world, device=rank, uid=obj[0])
+        d.run_batched(5, 2)          # graph mode: kernel + NCCL group per iteration, captured
+        d.run_stream(3)              # stream mode, same exchange
+        parts = [None] * world
+        dist.all_gather_object(parts, (d.lo, d.hi, d.local_temperature()))
+        d.close()
+        if rank == 0:
+            full = np.empty(shape, np.float32)
+            for a, b, arr in parts:
+                full[a:b] = arr
+            q.put(full)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape", [(64, 24, 8), (33, 40)])
+def test_multi_rank_nccl_halo_equals_single_gpu(gpu, shape):
+    n = _lib.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (one process per GPU)")
+    import torch.multiprocessing as mp
+
+    world = min(n, 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, shape, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    st = _state(shape)
+    want = wl.run_loop(wl.hotspot_program(), st, 13, dtype="f32").temperature
+    assert np.array_equal(got.astype(np.float64), want)

@@ -182,3 +182,33 @@ def test_time_workload_series(gpu):
     ph = wl.time_workload_phases(wl.vector_program(), w, plan, wl.ExecutionOrder.BATCHED, 3)
     assert all(c > 0 for c in ph["creation"]) and all(e > 0 for e in ph["execution"])
     assert all(t[0].nodes == 2 for t in ph["times"])
+
+
+def test_real_trace_is_consistent(gpu, tmp_path):
+    """Traced graph and stream runs: one record per kernel, ordered, in the reference schema."""
+    from paper_2501_09398_b200 import cli, trace as tr
+
+    state = cli.build_workload("hotspot2d", [256])
+    s = wl.DeviceSolver(state, "f32")
+    g = tr.capture_graph(s, 25, 4)
+    st = tr.capture_stream(s, 100)
+    assert g.kernels.shape == (100, 2) and st.kernels.shape == (100, 2)
+    for k in (g.kernels, st.kernels):
+        assert np.all(k[:, 1] >= k[:, 0]) and np.all(k[1:, 0] >= k[:-1, 0])
+    ts = [e[0] for e in g.events]
+    assert ts == sorted(ts)
+    kinds = {e[1] for e in g.events}
+    assert {"node_added", "graph_instantiated", "graph_uploaded", "graph_launched",
+            "kernel_started", "kernel_ended", "batch_gap_started"} <= kinds
+    p = tr.derive_parameters(g, st)
+    assert 0 < p["t_k"] < 1e-3 and p["t_i"] >= 0 and p["t_b"] >= 0 and p["k_c"] > 0
+    path = tmp_path / "g.csv"
+    tr.write_trace_csv(g, path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "# schema=1" and lines[1] == "timestamp,kind,batch_index,kernel_index"
+    # tracing off again: results unaffected, no records
+    ref = wl.state_checksum(wl.run_loop(wl.hotspot_program(), state, 10, dtype="f32"))
+    s.upload(state)
+    s.run_stream(10)
+    assert s.checksum() != 0 and wl.state_checksum(s.download(state)) == ref
+    s.close()
