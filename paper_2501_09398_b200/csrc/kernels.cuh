@@ -220,52 +220,73 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // chain. Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles
 // a y-row). grid = (ceil(M/V/256), rows).
 // ================================================================================================
-template <typename T, bool D3>
+template <typename T, bool D3, int R>
 __global__ void __launch_bounds__(256)
     k_hotspot_vec(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
                   int rows, int C, int L, T k, T loss, int has_top, int has_bot,
                   T *__restrict__ halo_up, T *__restrict__ halo_dn) {
+  // R consecutive rows per thread: the R+2 x-rows are loaded once (all loads independent and
+  // issued together), so L2->SM traffic for T drops from 3x to (R+2)/R x of the grid.
   constexpr int V = 16 / sizeof(T);
   pdl_trigger();
   const int64_t M = (int64_t)C * L;
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
-  const int i = blockIdx.y;
+  const int i0 = blockIdx.y * R;
   pdl_wait();
   TraceScope trace_scope_;
   if (m >= M) return;
-  const T *s = src + (int64_t)i * M + m;
-  T c[V], up[V], dn[V], ym[V], yp[V], pw[V];
-  ld16<T>(c, s);
-  if (i > 0 || has_top) ld16<T>(up, s - M); else for (int e = 0; e < V; ++e) up[e] = c[e];
-  if (i + 1 < rows || has_bot) ld16<T>(dn, s + M); else for (int e = 0; e < V; ++e) dn[e] = c[e];
-  ld16<T>(pw, power + (int64_t)i * M + m);
-  T out[V];
-  if (D3) {
-    const int j = (int)(m / L);
-    const int l = (int)(m - (int64_t)j * L);
-    if (j > 0) ld16<T>(ym, s - L); else for (int e = 0; e < V; ++e) ym[e] = c[e];
-    if (j < C - 1) ld16<T>(yp, s + L); else for (int e = 0; e < V; ++e) yp[e] = c[e];
-    const T zl = l > 0 ? s[-1] : c[0];
-    const T zr = l + V < L ? s[V] : c[V - 1];
+  const int nr = min(R, rows - i0);
+  T x[R + 2][V], pw[R][V];
+  const T *s = src + m;
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const T zm = e > 0 ? c[e - 1] : zl;
-      const T zp = e < V - 1 ? c[e + 1] : zr;
-      out[e] = hotspot_cell<T, true>(up[e], c[e], dn[e], ym[e], yp[e], zm, zp, pw[e], k, loss);
-    }
-  } else {
-    const T yl = m > 0 ? s[-1] : c[0];
-    const T yr = m + V < M ? s[V] : c[V - 1];
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const T a = e > 0 ? c[e - 1] : yl;
-      const T b = e < V - 1 ? c[e + 1] : yr;
-      out[e] = hotspot_cell<T, false>(up[e], c[e], dn[e], a, b, T(0), T(0), pw[e], k, loss);
-    }
+  for (int r = 0; r < R + 2; ++r) {
+    int q = i0 - 1 + r;
+    if (q >= i0 + nr + 1) q = i0 + nr;                      // past the chunk: never used
+    if (q < 0 && !has_top) q = 0;                            // edge clamp (np.pad "edge")
+    if (q >= rows && !has_bot) q = rows - 1;
+    ld16<T>(x[r], s + (int64_t)q * M);
   }
-  st16<T>(dst + (int64_t)i * M + m, out);
-  if (i == 0 && halo_up) st16<T>(halo_up + m, out);
-  if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r < nr) ld16<T>(pw[r], power + (int64_t)(i0 + r) * M + m);
+  int j = 0, l = 0;
+  if (D3) {
+    j = (int)(m / L);
+    l = (int)(m - (int64_t)j * L);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r >= nr) break;
+    const int i = i0 + r;
+    const T *si = s + (int64_t)i * M;
+    const T(&c)[V] = x[r + 1];
+    T out[V];
+    if (D3) {
+      T ym[V], yp[V];
+      if (j > 0) ld16<T>(ym, si - L); else for (int e = 0; e < V; ++e) ym[e] = c[e];
+      if (j < C - 1) ld16<T>(yp, si + L); else for (int e = 0; e < V; ++e) yp[e] = c[e];
+      const T zl = l > 0 ? si[-1] : c[0];
+      const T zr = l + V < L ? si[V] : c[V - 1];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const T zm = e > 0 ? c[e - 1] : zl;
+        const T zp = e < V - 1 ? c[e + 1] : zr;
+        out[e] = hotspot_cell<T, true>(x[r][e], c[e], x[r + 2][e], ym[e], yp[e], zm, zp, pw[r][e], k, loss);
+      }
+    } else {
+      const T yl = m > 0 ? si[-1] : c[0];
+      const T yr = m + V < M ? si[V] : c[V - 1];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const T a = e > 0 ? c[e - 1] : yl;
+        const T b = e < V - 1 ? c[e + 1] : yr;
+        out[e] = hotspot_cell<T, false>(x[r][e], c[e], x[r + 2][e], a, b, T(0), T(0), pw[r][e], k, loss);
+      }
+    }
+    st16<T>(dst + (int64_t)i * M + m, out);
+    if (i == 0 && halo_up) st16<T>(halo_up + m, out);
+    if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
+  }
 }
 
 // ---- bulk-copy (TMA) + mbarrier primitives ------------------------------------------------------

@@ -311,8 +311,25 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     dim3 block(256);
     switch (hotspot_variant<T>(c, rows)) {
       case HotKernel::Vec: {
-        const void *fn = d3 ? (const void *)ib::k_hotspot_vec<T, true> : (const void *)ib::k_hotspot_vec<T, false>;
-        dim3 grid((unsigned)((plane / V + 255) / 256), (unsigned)rows);
+        // rows per thread (R+2 row loads per R outputs): the smallest R whose grid fits in one
+        // wave of resident CTAs — a partial second wave costs a whole wave of latency on these
+        // launch-bound grids (measured: Hotspot3D 512x512x8 2048 CTAs -> 1024 CTAs, -8%).
+        // IB_HOTSPOT_VEC_ROWS overrides.
+        int64_t R = env_int("IB_HOTSPOT_VEC_ROWS", 0);
+        const int64_t threads_per_row = plane / V;
+        const int64_t xblocks = (threads_per_row + 255) / 256;
+        if (R <= 0) {
+          const int64_t slots = 8LL * c->num_sms;  // 256-thread CTAs, <= 32 regs -> 8 per SM
+          R = 1;
+          while (R < 4 && xblocks * ((rows + R - 1) / R) > slots) R *= 2;
+        }
+        R = R >= 4 ? 4 : (R >= 2 ? 2 : 1);
+        const void *fn;
+        if (d3) fn = R == 4 ? (const void *)ib::k_hotspot_vec<T, true, 4>
+                   : R == 2 ? (const void *)ib::k_hotspot_vec<T, true, 2> : (const void *)ib::k_hotspot_vec<T, true, 1>;
+        else fn = R == 4 ? (const void *)ib::k_hotspot_vec<T, false, 4>
+                  : R == 2 ? (const void *)ib::k_hotspot_vec<T, false, 2> : (const void *)ib::k_hotspot_vec<T, false, 1>;
+        dim3 grid((unsigned)xblocks, (unsigned)((rows + R - 1) / R));
         out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, k, loss,
                                   top, bot, up, dn));
         break;
