@@ -43,6 +43,8 @@ extern "C" {
 #define IB_SOLVER_HOTSPOT2D 1 /* hotspot_step 2-D   workloads.py:180-185 ; 1 kernel / iteration */
 #define IB_SOLVER_HOTSPOT3D 2 /* hotspot_step 3-D   workloads.py:186-204 ; 1 kernel / iteration */
 #define IB_SOLVER_FDTD 3      /* fdtd_h_step + fdtd_e_step workloads.py:325-413 ; 2 kernels / it. */
+#define IB_SOLVER_FDTD_FUSED 4 /* the same leapfrog as ONE kernel per iteration (H then E fused, fields
+                                  double-buffered: each field read and written once per iteration) */
 
 /* arithmetic type of the device state */
 #define IB_F32 0
@@ -134,6 +136,11 @@ int ib_graph_destroy(ib_ctx *ctx);
  * total T = T_C + T_E (Eq. 1) on the device clock; build_s / exec_s split it on the host clock. */
 int ib_run_batched(ib_ctx *ctx, int64_t batch_size, int64_t num_batches, int build_mode,
                    int flags, ib_times *times);
+/* Loop peeling (the reference rejects non-divisors, model.py:104-108): run
+ * total_iterations as floor(N/K) replays of a K-iteration graph plus one graph of the N mod K
+ * remainder iterations. Same timing convention as ib_run_batched (both builds inside gpu_s). */
+int ib_run_peeled(ib_ctx *ctx, int64_t total_iterations, int64_t batch_size, int build_mode,
+                  int flags, ib_times *times);
 int64_t ib_graph_batch_size(const ib_ctx *ctx);
 
 /* Device synchronisation of the context's streams. */

@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libiterbatch_b200.so")
 
 IB_OK, IB_EINVAL, IB_ECUDA, IB_ENOMEM, IB_ESTATE, IB_ENODEV = 0, -1, -2, -3, -4, -5
-SOLVER = {"vector": 0, "hotspot2d": 1, "hotspot3d": 2, "fdtd": 3}
+SOLVER = {"vector": 0, "hotspot2d": 1, "hotspot3d": 2, "fdtd": 3, "fdtd_fused": 4}
 DTYPE = {"f32": 0, "f64": 1}
 BUILD = {"manual": 0, "capture": 1}
 FLAG_PDL, FLAG_DEVICE_LAUNCH, FLAG_NO_UPLOAD, FLAG_WHILE, FLAG_MEMINFO = 0x1, 0x2, 0x4, 0x8, 0x10
@@ -69,6 +69,7 @@ PROTOTYPES = [
     ("ib_graph_run", _I, [_P, _I64, _T]),
     ("ib_graph_destroy", _I, [_P]),
     ("ib_run_batched", _I, [_P, _I64, _I64, _I, _I, _T]),
+    ("ib_run_peeled", _I, [_P, _I64, _I64, _I, _I, _T]),
     ("ib_graph_batch_size", _I64, [_P]),
     ("ib_sync", _I, [_P]),
     ("ib_host_alloc", _I, [ctypes.POINTER(_P), _SZ]),

@@ -170,6 +170,7 @@ struct ib_ctx {
   double scalars[3] = {0, 0, 0};
   std::vector<Slab> slabs;
   void *field[6] = {};      // vector / fdtd device fields (single slab)
+  void *field2[6] = {};     // fused fdtd: the second buffer of the ping-pong field pairs
   int64_t fshape[6][3] = {};
   int fndim[6] = {};
   int nfields = 0;
@@ -206,7 +207,13 @@ struct ib_ctx {
 
   cudaStream_t stream() const { return slabs[0].stream; }
   bool ping_pong() const {
-    return solver == IB_SOLVER_HOTSPOT2D || solver == IB_SOLVER_HOTSPOT3D;
+    return solver == IB_SOLVER_HOTSPOT2D || solver == IB_SOLVER_HOTSPOT3D ||
+           solver == IB_SOLVER_FDTD_FUSED;
+  }
+  bool fdtd() const { return solver == IB_SOLVER_FDTD || solver == IB_SOLVER_FDTD_FUSED; }
+  bool hotspot() const { return solver == IB_SOLVER_HOTSPOT2D || solver == IB_SOLVER_HOTSPOT3D; }
+  void *fieldp(int f, int parity) const {  // device field f holding parity `parity`
+    return (solver == IB_SOLVER_FDTD_FUSED && parity) ? field2[f] : field[f];
   }
   int64_t plane() const {  // elements per axis-0 plane (hotspot)
     return solver == IB_SOLVER_HOTSPOT3D ? dims[1] * dims[2] : dims[1];
@@ -417,6 +424,34 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
                             d, unit));
 }
 
+template <typename T>
+void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
+  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
+  const bool unit = c->scalars[0] == 1.0;
+  const void *fn = unit ? (const void *)ib::k_fdtd_fused<T, true> : (const void *)ib::k_fdtd_fused<T, false>;
+  const int64_t tiles = (int64_t)((nz + 1 + 31) / 32) * ((ny + 1 + 7) / 8);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+  const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
+  int64_t ppc = env_int("IB_FDTD_PPC", 0);
+  if (ppc <= 0) {  // x-chunks so the grid is about one wave of resident CTAs
+    const int64_t chunks = std::max<int64_t>(1, slots / tiles);
+    ppc = (nx + 1 + chunks - 1) / chunks;
+  }
+  ppc = std::max<int64_t>(1, std::min<int64_t>(ppc, nx + 1));
+  dim3 block(32, 8);
+  dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)((nx + 1 + ppc - 1) / ppc));
+  T *a[6], *b[6];
+  for (int f = 0; f < 6; ++f) {
+    a[f] = (T *)c->fieldp(f, parity);
+    b[f] = (T *)c->fieldp(f, parity ^ 1);
+  }
+  out.push_back(make_launch(fn, grid, block, 0, (const T *)a[0], (const T *)a[1], (const T *)a[2],
+                            (const T *)a[3], (const T *)a[4], (const T *)a[5], b[0], b[1], b[2], b[3],
+                            b[4], b[5], nx, ny, nz, (int)ppc, ch, ce, d));
+}
+
 void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
   out.clear();
   switch (c->solver) {
@@ -448,6 +483,12 @@ void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         fdtd_launches<float>(c, out);
       else
         fdtd_launches<double>(c, out);
+      break;
+    case IB_SOLVER_FDTD_FUSED:
+      if (c->dtype == IB_F32)
+        fdtd_fused_launches<float>(c, parity, out);
+      else
+        fdtd_fused_launches<double>(c, parity, out);
       break;
   }
 }
@@ -771,8 +812,10 @@ void ib_destroy(ib_ctx *c) {
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   if (!c->slabs.empty()) cudaSetDevice(c->slabs[0].device);
-  for (int f = 0; f < 6; ++f)
+  for (int f = 0; f < 6; ++f) {
     if (c->field[f]) cudaFree(c->field[f]);
+    if (c->field2[f]) cudaFree(c->field2[f]);
+  }
   if (c->d_counter) cudaFree(c->d_counter);
   if (c->d_trace) {
     ib::TraceBuf *none = nullptr;
@@ -788,7 +831,7 @@ void ib_destroy(ib_ctx *c) {
 
 static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   const int P = ndevices;
-  const bool hot = c->ping_pong();
+  const bool hot = c->solver == IB_SOLVER_HOTSPOT2D || c->solver == IB_SOLVER_HOTSPOT3D;
   if (P > 1 && !hot) return fail(IB_EINVAL, "multi-slab execution is only defined for hotspot solvers");
   const int64_t rows = hot ? c->dims[0] : 1;
   if (P > rows) return fail(IB_EINVAL, "more slabs than rows along axis 0");
@@ -848,6 +891,10 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
       const size_t b = (size_t)(numel(c->fshape[f], c->fndim[f]) * es);
       IB_CUDA(cudaMalloc(&c->field[f], b));
       IB_CUDA(cudaMemset(c->field[f], 0, b));
+      if (c->solver == IB_SOLVER_FDTD_FUSED) {
+        IB_CUDA(cudaMalloc(&c->field2[f], b));
+        IB_CUDA(cudaMemset(c->field2[f], 0, b));
+      }
     }
   }
   IB_CUDA(cudaDeviceSynchronize());
@@ -859,10 +906,10 @@ static int create_common(ib_ctx **out, int solver, int dtype, const int64_t *dim
                          int rank, int nranks, const void *id128) {
   if (!out) return fail(IB_EINVAL, "out is null");
   *out = nullptr;
-  if (solver < IB_SOLVER_VECTOR || solver > IB_SOLVER_FDTD) return fail(IB_EINVAL, "unknown solver");
+  if (solver < IB_SOLVER_VECTOR || solver > IB_SOLVER_FDTD_FUSED) return fail(IB_EINVAL, "unknown solver");
   if (dtype != IB_F32 && dtype != IB_F64) return fail(IB_EINVAL, "dtype must be IB_F32 or IB_F64");
-  static const int want_nd[4] = {1, 2, 3, 3};
-  static const int want_ns[4] = {1, 1, 1, 3};
+  static const int want_nd[5] = {1, 2, 3, 3, 3};
+  static const int want_ns[5] = {1, 1, 1, 3, 3};
   if (ndims != want_nd[solver] || !dims)
     return fail(IB_EINVAL, "solver expects " + std::to_string(want_nd[solver]) + " dims, got " + std::to_string(ndims));
   if (nscalars != want_ns[solver] || !scalars)
@@ -899,7 +946,7 @@ static int create_common(ib_ctx **out, int solver, int dtype, const int64_t *dim
   for (int i = 0; i < nscalars; ++i) c->scalars[i] = scalars[i];
   c->rank = rank;
   c->nranks = nranks;
-  if (solver == IB_SOLVER_FDTD && !(scalars[0] > 0.0)) {
+  if ((solver == IB_SOLVER_FDTD || solver == IB_SOLVER_FDTD_FUSED) && !(scalars[0] > 0.0)) {
     delete c;
     return fail(IB_EINVAL, "cell_size must be positive");
   }
@@ -907,7 +954,7 @@ static int create_common(ib_ctx **out, int solver, int dtype, const int64_t *dim
     c->nfields = 1;
     c->fndim[0] = 1;
     c->fshape[0][0] = dims[0];
-  } else if (solver == IB_SOLVER_FDTD) {
+  } else if (solver == IB_SOLVER_FDTD || solver == IB_SOLVER_FDTD_FUSED) {
     const int64_t nx = dims[0], ny = dims[1], nz = dims[2];
     const int64_t sh[6][3] = {{nx, ny + 1, nz + 1}, {nx + 1, ny, nz + 1}, {nx + 1, ny + 1, nz},
                               {nx + 1, ny, nz},     {nx, ny + 1, nz},     {nx, ny, nz + 1}};
@@ -984,8 +1031,8 @@ int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int
 int ib_slab_info(const ib_ctx *c, int64_t *lo, int64_t *hi, int *has_top, int *has_bot) {
   IB_TRY(check_ctx(c));
   const Slab &s = c->slabs[0];
-  if (lo) *lo = c->ping_pong() ? s.row_lo : 0;
-  if (hi) *hi = c->ping_pong() ? s.row_hi : c->dims[0];
+  if (lo) *lo = c->hotspot() ? s.row_lo : 0;
+  if (hi) *hi = c->hotspot() ? s.row_hi : c->dims[0];
   if (has_top) *has_top = c->nranks > 1 && s.has_top;
   if (has_bot) *has_bot = c->nranks > 1 && s.has_bot;
   return IB_OK;
@@ -1019,6 +1066,11 @@ int64_t ib_iteration_bytes(const ib_ctx *c) {
       for (int f = 0; f < 3; ++f) e += numel(c->fshape[f], 3);
       for (int f = 3; f < 6; ++f) h += numel(c->fshape[f], 3);
       return (e + 2 * h + h + 2 * e) * es;  // H half-step + E half-step
+    }
+    case IB_SOLVER_FDTD_FUSED: {
+      int64_t n = 0;
+      for (int f = 0; f < 6; ++f) n += numel(c->fshape[f], 3);
+      return 2 * n * es;  // every field read once and written once
     }
   }
   return -1;
@@ -1087,12 +1139,13 @@ static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
     return fail(IB_EINVAL, "field " + std::to_string(field) + " holds " + std::to_string(want) +
                                " bytes, got " + std::to_string(bytes));
   DeviceGuard guard;
-  if (c->ping_pong()) return hotspot_copy(c, field, host, bytes, up);
+  if (c->hotspot()) return hotspot_copy(c, field, host, bytes, up);
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  void *dev = c->fieldp(field, c->cur);
   if (up)
-    IB_CUDA(cudaMemcpyAsync(c->field[field], host, bytes, cudaMemcpyHostToDevice, c->stream()));
+    IB_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, c->stream()));
   else
-    IB_CUDA(cudaMemcpyAsync(host, c->field[field], bytes, cudaMemcpyDeviceToHost, c->stream()));
+    IB_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream()));
   IB_CUDA(cudaStreamSynchronize(c->stream()));
   return IB_OK;
 }
@@ -1244,7 +1297,7 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
   if (!c->exec[c->cur]) IB_TRY(build_one(c, c->cur, &t));
   if (c->ping_pong() && (c->K & 1) && !c->exec[c->cur ^ 1]) IB_TRY(build_one(c, c->cur ^ 1, &t));
   const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
-  const int64_t per = c->K * (c->solver == IB_SOLVER_FDTD ? 2 : (int64_t)c->slabs.size());
+  const int64_t per = c->K * (c->solver == IB_SOLVER_FDTD ? 2 : (int64_t)c->slabs.size());  // kernels / batch
   auto a = clk::now();
   IB_CUDA(cudaEventRecord(c->t0, c->stream()));
   if (num_batches > 0) {
@@ -1309,6 +1362,53 @@ int ib_run_batched(ib_ctx *c, int64_t batch_size, int64_t num_batches, int build
     tm->launches = r.launches;
     tm->build_s += r.build_s;  // lazily built parity executables, if any
   }
+  return IB_OK;
+}
+
+int ib_run_peeled(ib_ctx *c, int64_t total, int64_t batch_size, int build_mode, int flags,
+                  ib_times *tm) {
+  IB_TRY(check_ctx(c));
+  if (total < 0) return fail(IB_EINVAL, "total_iterations must be >= 0");
+  if (batch_size < 1) return fail(IB_EINVAL, "batch_size must be >= 1");
+  if (flags & IB_FLAG_WHILE) return fail(IB_EINVAL, "IB_FLAG_WHILE is not supported with peeling");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  IB_TRY(sync_all(c));
+  cudaEvent_t e0;
+  IB_CUDA(cudaEventCreate(&e0));
+  IB_CUDA(cudaEventRecord(e0, c->stream()));
+  ib_times acc = {};
+  const int64_t full = total / batch_size, rem = total % batch_size;
+  int rc = IB_OK;
+  for (int part = 0; part < 2 && rc == IB_OK; ++part) {
+    const int64_t k = part == 0 ? batch_size : rem;
+    const int64_t n = part == 0 ? full : 1;
+    if (k == 0 || n == 0) continue;
+    ib_times b = {}, r = {};
+    rc = ib_graph_build(c, k, build_mode, flags, &b);
+    if (rc == IB_OK) rc = ib_graph_run(c, n, &r);
+    acc.create_s += b.create_s;
+    acc.instantiate_s += b.instantiate_s;
+    acc.upload_s += b.upload_s;
+    acc.build_s += b.build_s + r.build_s;
+    acc.exec_s += r.exec_s;
+    acc.kernels += r.kernels;
+    acc.launches += r.launches;
+    acc.nodes += b.nodes;
+  }
+  if (rc != IB_OK) {
+    cudaEventDestroy(e0);
+    return rc;
+  }
+  IB_CUDA(cudaEventRecord(c->t1, c->stream()));
+  IB_CUDA(cudaEventSynchronize(c->t1));
+  float ms = 0;
+  cudaError_t e = cudaEventElapsedTime(&ms, e0, c->t1);
+  cudaEventDestroy(e0);
+  IB_CUDA(e);
+  free_graphs(c);
+  acc.gpu_s = ms * 1e-3;
+  if (tm) *tm = acc;
   return IB_OK;
 }
 

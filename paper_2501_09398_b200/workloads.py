@@ -59,6 +59,7 @@ __all__ = [
     "te101_cavity",
     "run_loop",
     "run_batched",
+    "run_peeled",
     "time_workload",
     "time_workload_phases",
     "state_checksum",
@@ -324,8 +325,11 @@ class DeviceSolver:
         instantiated/uploaded once and replayed.
     """
 
-    def __init__(self, state, dtype="f64", devices=None, upload: bool = True):
+    def __init__(self, state, dtype="f64", devices=None, upload: bool = True, fuse: bool = False):
         self.kind = _kind_of_state(state)
+        self.fused = bool(fuse)
+        if self.fused and self.kind != "fdtd":
+            raise ValueError("fuse=True applies to FDTD (H and E half-steps in one kernel)")
         self.dtype = _norm_dtype(dtype)
         self.np_dtype = _NP_DTYPE[self.dtype]
         self.dims, self.scalars = _dims_scalars(self.kind, state)
@@ -337,7 +341,8 @@ class DeviceSolver:
         sc = (ctypes.c_double * len(self.scalars))(*self.scalars)
         dv = (ctypes.c_int * max(1, len(devs)))(*(devs or [0]))
         _lib.check(
-            L.ib_create(ctypes.byref(ctx), _lib.SOLVER[self.kind], _lib.DTYPE[self.dtype], dims,
+            L.ib_create(ctypes.byref(ctx), _lib.SOLVER["fdtd_fused" if self.fused else self.kind],
+                        _lib.DTYPE[self.dtype], dims,
                         len(self.dims), sc, len(self.scalars), dv if devs else None, len(devs))
         )
         self._ctx = ctx
@@ -459,6 +464,15 @@ class DeviceSolver:
                                              _lib.BUILD[build], flags, ctypes.byref(t)))
         return Times.from_c(t)
 
+    def run_peeled(self, total_iterations: int, batch_size: int, build: str = "manual",
+                   pdl: bool = False) -> Times:
+        """floor(N/K) replays of a K-iteration graph + one remainder graph (loop peeling)."""
+        t = _lib.IbTimes()
+        _lib.check(_lib.lib().ib_run_peeled(self.ctx, int(total_iterations), int(batch_size),
+                                            _lib.BUILD[build], _lib.FLAG_PDL if pdl else 0,
+                                            ctypes.byref(t)))
+        return Times.from_c(t)
+
     def run_graph(self, num_batches: int) -> Times:
         t = _lib.IbTimes()
         _lib.check(_lib.lib().ib_graph_run(self.ctx, int(num_batches), ctypes.byref(t)))
@@ -480,7 +494,7 @@ class DeviceSolver:
 
     @property
     def kernels_per_iteration(self) -> int:
-        n = 2 if self.kind == "fdtd" else 1
+        n = 2 if (self.kind == "fdtd" and not getattr(self, "fused", False)) else 1
         return n * max(1, len(self.devices))
 
     def checksum(self) -> int:
@@ -508,19 +522,19 @@ _CACHE: "OrderedDict[tuple, DeviceSolver]" = OrderedDict()
 _CACHE_SIZE = 2
 
 
-def _solver_for(state, dtype, devices) -> DeviceSolver:
+def _solver_for(state, dtype, devices, fuse: bool = False) -> DeviceSolver:
     """A (cached) device context for this state's shape, with the state uploaded."""
     kind = _kind_of_state(state)
     dt = _norm_dtype(dtype)
     dims, scalars = _dims_scalars(kind, state)
     devs = tuple(devices) if devices else ()
-    key = (kind, dt, dims, scalars, devs)
+    key = (kind, dt, dims, scalars, devs, bool(fuse))
     s = _CACHE.pop(key, None)
     if s is None:
         while len(_CACHE) >= _CACHE_SIZE:
             _, old = _CACHE.popitem(last=False)
             old.close()
-        s = DeviceSolver(state, dt, devs, upload=False)
+        s = DeviceSolver(state, dt, devs, upload=False, fuse=fuse)
     _CACHE[key] = s
     s.upload(state)
     return s
@@ -621,7 +635,7 @@ def _check_program(program, state) -> str:
 # Drivers
 # ================================================================================================
 def run_loop(program, state, total_iterations: int, workers=None, *, dtype="f64", devices=None,
-             pdl: bool = False):
+             pdl: bool = False, fuse: bool = False):
     """Apply the program total_iterations times, one launch at a time (Listing 1).
 
     Mirrors workloads.py:442-450: N = 0 returns the same state; N < 0 raises ValueError.
@@ -632,13 +646,14 @@ def run_loop(program, state, total_iterations: int, workers=None, *, dtype="f64"
     _check_program(program, state)
     if total == 0:
         return state
-    s = _solver_for(state, dtype, devices)
+    s = _solver_for(state, dtype, devices, fuse)
     s.run_stream(total, pdl=pdl)
     return s.download(state, fields=_written_fields(state))
 
 
 def run_batched(program, state, batch_size: int, num_batches: int, workers=None, *, dtype="f64",
-                devices=None, build: str = "manual", pdl: bool = False, while_loop: bool = False):
+                devices=None, build: str = "manual", pdl: bool = False, while_loop: bool = False,
+                fuse: bool = False):
     """Apply the program in num_batches replays of a batch_size-iteration CUDA graph (Listing 3).
 
     Mirrors workloads.py:453-471 (batch_size < 1 or num_batches < 0 raise ValueError) and
@@ -653,10 +668,31 @@ def run_batched(program, state, batch_size: int, num_batches: int, workers=None,
     _check_program(program, state)
     if num == 0:
         return state
-    s = _solver_for(state, dtype, devices)
+    s = _solver_for(state, dtype, devices, fuse)
     s.build_graph(size, build=build, pdl=pdl, while_loop=while_loop)
     s.run_graph(num)
     s.destroy_graph()
+    return s.download(state, fields=_written_fields(state))
+
+
+def run_peeled(program, state, total_iterations: int, batch_size: int, workers=None, *,
+               dtype="f64", devices=None, build: str = "manual", pdl: bool = False):
+    """Any total_iterations with any batch_size: floor(N/K) graph replays plus a remainder graph.
+
+    Loop peeling, the paper's remedy for the divisibility restriction that the
+    reference's BatchPlan enforces (model.py:104-108). Bit-identical to run_loop(N).
+    """
+    total = operator.index(total_iterations)
+    size = operator.index(batch_size)
+    if total < 0:
+        raise ValueError("total_iterations must be >= 0")
+    if size < 1:
+        raise ValueError("batch_size must be >= 1")
+    _check_program(program, state)
+    if total == 0:
+        return state
+    s = _solver_for(state, dtype, devices)
+    s.run_peeled(total, size, build=build, pdl=pdl)
     return s.download(state, fields=_written_fields(state))
 
 

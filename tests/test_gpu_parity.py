@@ -235,3 +235,28 @@ def test_steps_match_reference_fixtures(gpu, fixtures):
     g = wl.run_batched(wl.fdtd_program(), f, 4, 3)
     for n in names:
         assert np.array_equal(getattr(g, n), fixtures["fdtd_out12_" + n]), n
+
+
+@pytest.mark.parametrize("case", [("vector", "1001", 37, 5), ("hotspot2d", "33,17", 23, 4),
+                                  ("hotspot3d", "9,7,8", 11, 3), ("fdtd", "6,5,7", 13, 6),
+                                  ("hotspot2d", "20,12", 7, 9)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_loop_peeling_equals_loop(gpu, case, dtype):
+    """Non-divisible N: floor(N/K) batches + remainder == run_loop(N), bitwise."""
+    name, size, n, k = case
+    state = cli.build_workload(name, _sizes(size))
+    prog = _program(name)
+    ref = wl.state_checksum(wl.run_loop(prog, state, n, dtype=dtype))
+    for build in ("manual", "capture"):
+        got = wl.state_checksum(wl.run_peeled(prog, state, n, k, dtype=dtype, build=build, pdl=True))
+        assert got == ref, build
+
+
+@pytest.mark.parametrize("kat", [k for k in KATS if k["workload"] == "fdtd"],
+                         ids=[_kat_id(k) for k in KATS if k["workload"] == "fdtd"])
+def test_p0_fused_fdtd_matches_reference(gpu, kat):
+    """The fused one-kernel-per-iteration FDTD reproduces the reference checksums too."""
+    state = _state(kat)
+    n, k = kat["iterations"], kat["batch_size"]
+    out = wl.run_batched(_program("fdtd"), state, k, n // k, fuse=True, pdl=True)
+    assert f"{wl.state_checksum(out):016x}" == kat["checksum"]

@@ -112,3 +112,27 @@ def test_fdtd_non_unit_cell_size(gpu, env):
         got = wl.run_loop(wl.fdtd_program(), w, 9)
         for g, ww in zip(got.state_arrays(), want):
             assert np.array_equal(g, ww)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("ppc", [0, 1, 2, 3])
+@pytest.mark.parametrize("dims", FDTD_DIMS + [(40, 9, 70), (7, 17, 31)],
+                         ids=["x".join(map(str, d)) for d in FDTD_DIMS + [(40, 9, 70), (7, 17, 31)]])
+def test_fdtd_fused_bitwise(gpu, env, dims, ppc, dtype):
+    """One kernel per iteration (H then E fused, double-buffered fields) == the oracle, bitwise."""
+    env(IB_FDTD_PPC=ppc)
+    base = wl.fdtd_cavity(*dims)
+    rng = np.random.default_rng(sum(dims) * 7 + ppc)
+    state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
+                            base.cell_size, base.time_step)
+    npd = np.float32 if dtype == "f32" else np.float64
+    dt = state.time_step
+    want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
+                     dt / wl.VACUUM_PERMITTIVITY, 5, npd)
+    for kw in ({"build": "manual"}, {"build": "capture", "pdl": True}):
+        got = wl.run_batched(wl.fdtd_program(), state, 5, 1, dtype=dtype, fuse=True, **kw)  # odd K
+        for g, w in zip(got.state_arrays(), want):
+            assert np.array_equal(np.asarray(g, npd), w)
+    got = wl.run_loop(wl.fdtd_program(), state, 5, dtype=dtype, fuse=True)
+    for g, w in zip(got.state_arrays(), want):
+        assert np.array_equal(np.asarray(g, npd), w)
