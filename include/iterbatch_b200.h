@@ -174,11 +174,12 @@ int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int
 int ib_slab_info(const ib_ctx *ctx, int64_t *lo, int64_t *hi, int *has_top, int *has_bot);
 
 /* ---- real traces (the reference's EventTrace schema, simulate.py:28-36, fileio.py:48) ---------
- * ib_trace_enable(ctx, capacity > 0) clears and arms tracing for up to `capacity` kernels; 0 disarms.
- * While armed (single-slab contexts; one traced context per device at a time) every kernel records
- * its grid's [start, end] from %globaltimer, mapped onto the host steady clock (calibrated at arm
- * time, about +-5 us), and the runtime logs host events: node added (0), graph instantiated (1),
- * graph uploaded (2), graph launched (3), baseline kernel launched (7), build started (100).
+ * ib_trace_enable(ctx, capacity > 0) clears and arms tracing; 0 disarms. While armed (single-slab
+ * contexts; one traced context per process at a time) CUPTI activity tracing (libcupti, dlopen'ed —
+ * the mechanism nsys uses; the kernels carry no instrumentation) records every solver kernel's
+ * [start, end] in ns, and the runtime logs host events on the same CUPTI timebase: node added (0),
+ * graph instantiated (1), graph uploaded (2), graph launched (3), baseline kernel launched (7),
+ * build started (100).
  * ib_trace_kernels returns the number of kernels recorded and copies [start_ns, end_ns] pairs;
  * ib_trace_host_events returns the number of host events and copies (t_ns, kind, batch, kernel). */
 #define IB_EV_NODE_ADDED 0

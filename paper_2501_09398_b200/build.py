@@ -28,6 +28,7 @@ NVCC_FLAGS = [
     # IEEE division / sqrt
     "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
     "--cudart", "static",
+    "-ldl",
     "-I", os.path.join(ROOT, "include"),
 ]
 

@@ -36,52 +36,6 @@ template <> struct rn<double> {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
 
-// ---- real-trace capture (timelines in the reference's EventTrace schema) --------
-// When a context enables tracing, c_trace points at a TraceBuf and every kernel records its grid's
-// [first CTA start, last CTA end] in %globaltimer ns: thread 0 of each CTA folds its start/end in
-// with atomicMin/atomicMax, and the last CTA to finish appends the pair and resets the
-// accumulators (the next kernel cannot start before this grid completed: stream order or
-// griddepcontrol.wait). Off (nullptr) it costs one uniform constant load and a branch.
-struct TraceBuf {
-  unsigned long long start, end;
-  unsigned int done, seq, cap, pad;
-  unsigned long long rec[2];  // 2*cap entries follow
-};
-__constant__ TraceBuf *c_trace;
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-struct TraceScope {
-  __device__ __forceinline__ TraceScope() {
-    TraceBuf *tb = c_trace;
-    if (tb && threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) atomicMin(&tb->start, gtimer());
-  }
-  __device__ __forceinline__ ~TraceScope() {
-    TraceBuf *tb = c_trace;
-    if (!tb || threadIdx.x != 0 || threadIdx.y != 0 || threadIdx.z != 0) return;
-    atomicMax(&tb->end, gtimer());
-    __threadfence();
-    const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
-    if (atomicAdd(&tb->done, 1u) == total - 1) {
-      __threadfence();
-      const unsigned int s = tb->seq;
-      if (s < tb->cap) {
-        tb->rec[2 * s] = atomicAdd(&tb->start, 0ull);
-        tb->rec[2 * s + 1] = atomicAdd(&tb->end, 0ull);
-      }
-      tb->seq = s + 1;
-      tb->start = ~0ull;
-      tb->end = 0ull;
-      tb->done = 0u;
-      __threadfence();
-    }
-  }
-};
-
 // ================================================================================================
 // Skeleton: vector scale, in place.  workloads.py:97-105  out = values * c
 //   binary64: v' = v (*) c
@@ -92,7 +46,6 @@ struct TraceScope {
 __global__ void __launch_bounds__(256) k_vector_f32(float *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
-  TraceScope trace_scope_;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n4 = n >> 2;
   if (i < n4) {
@@ -111,7 +64,6 @@ __global__ void __launch_bounds__(256) k_vector_f32(float *__restrict__ v, int64
 __global__ void __launch_bounds__(256) k_vector_f64(double *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
-  TraceScope trace_scope_;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n2 = n >> 1;
   if (i < n2) {
@@ -153,7 +105,6 @@ __global__ void __launch_bounds__(256)
   const int i0 = blockIdx.y * rows_per_chunk;
   const int i1 = min(rows, i0 + rows_per_chunk);
   pdl_wait();
-  TraceScope trace_scope_;
   if (p >= plane || i0 >= rows) return;
   const int j = D3 ? (int)(p / L) : (int)p;
   const int l = D3 ? (int)(p - (int64_t)j * L) : 0;
@@ -233,7 +184,6 @@ __global__ void __launch_bounds__(256)
   const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
   const int i0 = blockIdx.y * R;
   pdl_wait();
-  TraceScope trace_scope_;
   if (m >= M) return;
   const int nr = min(R, rows - i0);
   T x[R + 2][V], pw[R][V];
@@ -365,7 +315,6 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   pdl_wait();  // from here on the previous kernel's writes are visible
-  TraceScope trace_scope_;
   auto issue = [&](int t) {
     const int s = t % nstages;
     int q = i0 - 1 + t;
@@ -486,7 +435,6 @@ __global__ void __launch_bounds__(256)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   pdl_wait();
-  TraceScope trace_scope_;
   if (p >= (int64_t)(ny + 1) * pw) return;
   const int j = (int)(p / pw);
   const int k = (int)(p - (int64_t)j * pw);
@@ -525,7 +473,6 @@ __global__ void __launch_bounds__(256)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   pdl_wait();
-  TraceScope trace_scope_;
   if (p >= (int64_t)(ny + 1) * pw) return;
   const int j = (int)(p / pw);
   const int k = (int)(p - (int64_t)j * pw);
@@ -584,7 +531,6 @@ __global__ void __launch_bounds__(256)
   const int i0 = blockIdx.y * planes_per_cta;
   const int i1 = min(nx + 1, i0 + planes_per_cta);
   pdl_wait();
-  TraceScope trace_scope_;
   if (p >= (ny + 1) * pw) return;
   const int j = p / pw;
   const int k = p - j * pw;
@@ -627,7 +573,6 @@ __global__ void __launch_bounds__(256)
   const int i0 = blockIdx.y * planes_per_cta;
   const int i1 = min(nx + 1, i0 + planes_per_cta);
   pdl_wait();
-  TraceScope trace_scope_;
   if (p >= (ny + 1) * pw) return;
   const int j = p / pw;
   const int k = p - j * pw;
@@ -704,7 +649,6 @@ __global__ void __launch_bounds__(256)
   const int j = blockIdx.y * 8 + threadIdx.y;
   const int i = blockIdx.z;
   pdl_wait();
-  TraceScope trace_scope_;
   if (k > nz || j > ny) return;
   const int nz1 = nz + 1, ny1 = ny + 1;
   const int A = (i * ny1 + j) * nz1 + k;
@@ -740,7 +684,6 @@ __global__ void __launch_bounds__(256)
   const int j = blockIdx.y * 8 + threadIdx.y;
   const int i = blockIdx.z;
   pdl_wait();
-  TraceScope trace_scope_;
   if (k > nz || j > ny) return;
   const int nz1 = nz + 1, ny1 = ny + 1;
   const int A = (i * ny1 + j) * nz1 + k;
@@ -808,7 +751,6 @@ __global__ void __launch_bounds__(256)
   const int ib = i0 > 0 ? i0 - 1 : 0;
   const int ny1 = ny + 1, nz1 = nz + 1;
   pdl_wait();
-  TraceScope trace_scope_;
 
   // E tile element e (0..3*ECELLS) -> (component, y, z); returns the global offset or -1
   auto e_off = [&](int e, int i, int &c, int &ej, int &ek) -> int64_t {

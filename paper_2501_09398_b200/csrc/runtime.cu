@@ -12,7 +12,10 @@
 //                                          halo planes pushed by the stencil kernel itself
 // The state lives in HBM for the whole run; the boundary is crossed by ib_upload/ib_download.
 #include <cuda_runtime.h>
+#include <cupti_activity.h>
 #include <dlfcn.h>
+
+#include <mutex>
 
 #include <algorithm>
 #include <chrono>
@@ -161,6 +164,62 @@ Nccl &nccl() {
 }
 constexpr int kNcclInt8 = 0;  // ncclInt8: halo planes move as raw bytes
 
+// ---- CUPTI activity tracing, loaded at run time (what nsys uses; no in-kernel instrumentation) -
+struct Cupti {
+  bool ok = false;
+  std::string err;
+  CUptiResult (*RegisterCallbacks)(CUpti_BuffersCallbackRequestFunc, CUpti_BuffersCallbackCompleteFunc) = nullptr;
+  CUptiResult (*Enable)(CUpti_ActivityKind) = nullptr;
+  CUptiResult (*Disable)(CUpti_ActivityKind) = nullptr;
+  CUptiResult (*FlushAll)(uint32_t) = nullptr;
+  CUptiResult (*GetNextRecord)(uint8_t *, size_t, CUpti_Activity **) = nullptr;
+  CUptiResult (*GetTimestamp)(uint64_t *) = nullptr;
+  std::mutex mu;
+  std::vector<int64_t> kernels;  // (start, end) pairs of this library's solver kernels
+};
+Cupti &cupti() {
+  static Cupti *c = [] {
+    Cupti *r = new Cupti();
+    void *h = dlopen("libcupti.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcupti.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      r->err = std::string("dlopen(libcupti) failed: ") + dlerror();
+      return r;
+    }
+    r->RegisterCallbacks = (decltype(r->RegisterCallbacks))dlsym(h, "cuptiActivityRegisterCallbacks");
+    r->Enable = (decltype(r->Enable))dlsym(h, "cuptiActivityEnable");
+    r->Disable = (decltype(r->Disable))dlsym(h, "cuptiActivityDisable");
+    r->FlushAll = (decltype(r->FlushAll))dlsym(h, "cuptiActivityFlushAll");
+    r->GetNextRecord = (decltype(r->GetNextRecord))dlsym(h, "cuptiActivityGetNextRecord");
+    r->GetTimestamp = (decltype(r->GetTimestamp))dlsym(h, "cuptiGetTimestamp");
+    r->ok = r->RegisterCallbacks && r->Enable && r->Disable && r->FlushAll && r->GetNextRecord &&
+            r->GetTimestamp;
+    if (!r->ok) r->err = "libcupti lacks a required symbol";
+    return r;
+  }();
+  return *c;
+}
+void CUPTIAPI cupti_buffer_requested(uint8_t **buffer, size_t *size, size_t *max_records) {
+  *size = 8u << 20;
+  *buffer = (uint8_t *)aligned_alloc(8, *size);
+  *max_records = 0;
+}
+void CUPTIAPI cupti_buffer_completed(CUcontext, uint32_t, uint8_t *buffer, size_t, size_t valid) {
+  Cupti &c = cupti();
+  CUpti_Activity *rec = nullptr;
+  std::lock_guard<std::mutex> lock(c.mu);
+  while (c.GetNextRecord(buffer, valid, &rec) == CUPTI_SUCCESS) {
+    if (rec->kind != CUPTI_ACTIVITY_KIND_CONCURRENT_KERNEL && rec->kind != CUPTI_ACTIVITY_KIND_KERNEL) continue;
+    const CUpti_ActivityKernel9 *k = (const CUpti_ActivityKernel9 *)rec;
+    const char *n = k->name ? k->name : "";
+    // the solver kernels live in namespace ib (mangled _ZN2ib...); utilities are not traced
+    if (std::strncmp(n, "_ZN2ib", 6) != 0 || std::strstr(n, "k_flush")) continue;
+    c.kernels.push_back((int64_t)k->start);
+    c.kernels.push_back((int64_t)k->end);
+  }
+  free(buffer);
+}
+
 }  // namespace
 
 struct ib_ctx {
@@ -191,19 +250,12 @@ struct ib_ctx {
   int rank = 0, nranks = 1;
   void *comm = nullptr;  // ncclComm_t
   bool dist() const { return comm != nullptr; }
-  // tracing
-  ib::TraceBuf *d_trace = nullptr;
+  // tracing (CUPTI activity records; host events on the CUPTI timebase)
+  bool tracing = false;
   int64_t trace_cap = 0;
-  int64_t gpu_to_host_ns = 0;  // host_ns = gpu_ns + offset
   struct HostEv { int64_t t, kind, batch, kernel; };
   std::vector<HostEv> host_ev;
-  bool tracing() const { return d_trace != nullptr; }
-  void ev(int kind, int64_t batch = -1, int64_t kernel = -1) {
-    if (!d_trace) return;
-    const int64_t t = std::chrono::duration_cast<std::chrono::nanoseconds>(
-                          std::chrono::steady_clock::now().time_since_epoch()).count();
-    host_ev.push_back({t, kind, batch, kernel});
-  }
+  void ev(int kind, int64_t batch = -1, int64_t kernel = -1);
 
   cudaStream_t stream() const { return slabs[0].stream; }
   bool ping_pong() const {
@@ -219,6 +271,13 @@ struct ib_ctx {
     return solver == IB_SOLVER_HOTSPOT3D ? dims[1] * dims[2] : dims[1];
   }
 };
+
+void ib_ctx::ev(int kind, int64_t batch, int64_t kernel) {
+  if (!tracing) return;
+  uint64_t t = 0;
+  cupti().GetTimestamp(&t);
+  host_ev.push_back({(int64_t)t, kind, batch, kernel});
+}
 
 namespace {
 
@@ -817,10 +876,12 @@ void ib_destroy(ib_ctx *c) {
     if (c->field2[f]) cudaFree(c->field2[f]);
   }
   if (c->d_counter) cudaFree(c->d_counter);
-  if (c->d_trace) {
-    ib::TraceBuf *none = nullptr;
-    cudaMemcpyToSymbol(ib::c_trace, &none, sizeof(none));
-    cudaFree(c->d_trace);
+  if (c->tracing) {
+    Cupti &cp = cupti();
+    cp.Disable(CUPTI_ACTIVITY_KIND_CONCURRENT_KERNEL);
+    cp.FlushAll(1);
+    std::lock_guard<std::mutex> lock(cp.mu);
+    cp.kernels.clear();
   }
   if (c->flush) cudaFree(c->flush);
   if (c->t0) cudaEventDestroy(c->t0);
@@ -1447,76 +1508,61 @@ uint64_t ib_fnv1a64_f64(const void *values, size_t n, int dtype, uint64_t h) {
   return h;
 }
 
-__global__ void k_clock(unsigned long long *out) { *out = ib::gtimer(); }
-
 int ib_trace_enable(ib_ctx *c, int64_t capacity) {
   IB_TRY(check_ctx(c));
   if (capacity < 0) return fail(IB_EINVAL, "capacity must be >= 0");
   if (capacity > 0 && c->slabs.size() > 1) return fail(IB_EINVAL, "tracing needs a single-slab context");
+  Cupti &cp = cupti();
+  if (!cp.ok) return fail(IB_ECUDA, cp.err);
   DeviceGuard guard;
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
   IB_TRY(sync_all(c));
-  ib::TraceBuf *none = nullptr;
-  IB_CUDA(cudaMemcpyToSymbol(ib::c_trace, &none, sizeof(none)));
-  if (c->d_trace) cudaFree(c->d_trace);
-  c->d_trace = nullptr;
-  c->trace_cap = 0;
-  c->host_ev.clear();
-  if (capacity == 0) return IB_OK;
-  const size_t bytes = sizeof(ib::TraceBuf) + (size_t)capacity * 2 * sizeof(unsigned long long);
-  IB_CUDA(cudaMalloc(&c->d_trace, bytes));
-  ib::TraceBuf init = {};
-  init.start = ~0ull;
-  init.cap = (unsigned)std::min<int64_t>(capacity, 0x7fffffff);
-  IB_CUDA(cudaMemcpy(c->d_trace, &init, sizeof(init), cudaMemcpyHostToDevice));
-  // map %globaltimer onto the host steady clock: the narrowest of 16 launch round trips
-  unsigned long long *d_t = nullptr, g = 0;
-  IB_CUDA(cudaMalloc(&d_t, sizeof(*d_t)));
-  int64_t best_w = INT64_MAX;
-  for (int r = 0; r < 16; ++r) {
-    const int64_t h0 = std::chrono::duration_cast<std::chrono::nanoseconds>(
-                           clk::now().time_since_epoch()).count();
-    k_clock<<<1, 1, 0, c->stream()>>>(d_t);
-    cudaError_t e = cudaStreamSynchronize(c->stream());
-    const int64_t h1 = std::chrono::duration_cast<std::chrono::nanoseconds>(
-                           clk::now().time_since_epoch()).count();
-    if (e != cudaSuccess) {
-      cudaFree(d_t);
-      IB_CUDA(e);
-    }
-    IB_CUDA(cudaMemcpy(&g, d_t, sizeof(g), cudaMemcpyDeviceToHost));
-    if (h1 - h0 < best_w) {
-      best_w = h1 - h0;
-      c->gpu_to_host_ns = (h0 + h1) / 2 - (int64_t)g;
-    }
+  static bool registered = false;
+  if (!registered) {
+    if (cp.RegisterCallbacks(cupti_buffer_requested, cupti_buffer_completed) != CUPTI_SUCCESS)
+      return fail(IB_ECUDA, "cuptiActivityRegisterCallbacks failed");
+    registered = true;
   }
-  cudaFree(d_t);
+  if (c->tracing) {
+    cp.Disable(CUPTI_ACTIVITY_KIND_CONCURRENT_KERNEL);
+    cp.FlushAll(1);
+  }
+  {
+    std::lock_guard<std::mutex> lock(cp.mu);
+    cp.kernels.clear();
+  }
+  c->host_ev.clear();
+  c->tracing = false;
+  c->trace_cap = 0;
+  if (capacity == 0) return IB_OK;
+  if (cp.Enable(CUPTI_ACTIVITY_KIND_CONCURRENT_KERNEL) != CUPTI_SUCCESS)
+    return fail(IB_ECUDA, "cuptiActivityEnable(CONCURRENT_KERNEL) failed");
+  c->tracing = true;
   c->trace_cap = capacity;
-  IB_CUDA(cudaMemcpyToSymbol(ib::c_trace, &c->d_trace, sizeof(c->d_trace)));
   return IB_OK;
 }
 
 int64_t ib_trace_kernels(ib_ctx *c, int64_t *out, int64_t capacity) {
-  if (!c || !c->d_trace) return fail(IB_ESTATE, "tracing is not enabled");
+  if (!c || !c->tracing) return fail(IB_ESTATE, "tracing is not enabled");
   DeviceGuard guard;
   cudaSetDevice(c->slabs[0].device);
   if (sync_all(c) != IB_OK) return IB_ECUDA;
-  ib::TraceBuf hdr;
-  if (cudaMemcpy(&hdr, c->d_trace, sizeof(hdr), cudaMemcpyDeviceToHost) != cudaSuccess)
-    return fail(IB_ECUDA, "trace header copy failed");
-  const int64_t n = std::min<int64_t>(std::min<int64_t>(hdr.seq, c->trace_cap), capacity);
-  if (out && n > 0) {
-    std::vector<unsigned long long> buf((size_t)n * 2);
-    if (cudaMemcpy(buf.data(), c->d_trace->rec, buf.size() * sizeof(unsigned long long),
-                   cudaMemcpyDeviceToHost) != cudaSuccess)
-      return fail(IB_ECUDA, "trace record copy failed");
-    for (int64_t i = 0; i < 2 * n; ++i) out[i] = (int64_t)buf[(size_t)i] + c->gpu_to_host_ns;
+  Cupti &cp = cupti();
+  cp.FlushAll(1);
+  std::lock_guard<std::mutex> lock(cp.mu);
+  std::vector<std::pair<int64_t, int64_t>> k;
+  for (size_t i = 0; i + 1 < cp.kernels.size(); i += 2) k.push_back({cp.kernels[i], cp.kernels[i + 1]});
+  std::sort(k.begin(), k.end());
+  const int64_t n = (int64_t)k.size();
+  for (int64_t i = 0; out && i < std::min(n, capacity); ++i) {
+    out[2 * i] = k[(size_t)i].first;
+    out[2 * i + 1] = k[(size_t)i].second;
   }
-  return (int64_t)hdr.seq;
+  return n;
 }
 
 int64_t ib_trace_host_events(ib_ctx *c, int64_t *rows, int64_t capacity) {
-  if (!c || !c->d_trace) return fail(IB_ESTATE, "tracing is not enabled");
+  if (!c || !c->tracing) return fail(IB_ESTATE, "tracing is not enabled");
   const int64_t n = (int64_t)c->host_ev.size();
   for (int64_t i = 0; rows && i < std::min(n, capacity); ++i) {
     rows[4 * i] = c->host_ev[(size_t)i].t;

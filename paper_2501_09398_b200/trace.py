@@ -4,9 +4,10 @@ The reference only *simulates* the Fig. 1 timelines (pkg/src/iterbatch/simulate.
 reads measured platform constants from a ``key = value`` params file (fileio.py:34-45,70-125).
 This module records the real thing:
 
-* ``capture_graph`` / ``capture_stream`` arm the runtime's trace (``ib_trace_enable``): every
-  kernel's grid [start, end] from %globaltimer, mapped onto the host steady clock, plus the host
-  events of the build and launch calls;
+* ``capture_graph`` / ``capture_stream`` arm the runtime's trace (``ib_trace_enable``): CUPTI
+  activity records give every solver kernel's [start, end] (the mechanism nsys uses; the kernels
+  carry no instrumentation), and the host events of the build and launch calls are stamped on the
+  same CUPTI timebase;
 * ``write_trace_csv`` writes them in the reference trace-CSV schema (``# schema=1``,
   ``timestamp,kind,batch_index,kernel_index``, 9-decimal seconds, fileio.py:48,193-205), with the
   clock starting at zero at the build start as the simulator's does; ``iterbatch``'s
