@@ -73,8 +73,9 @@ struct Launch {
   size_t smem = 0;  // dynamic shared memory bytes
   int slab = 0;
   int nargs = 0;
-  alignas(16) unsigned char slot[16][16];
-  void *ptr[16];
+  static constexpr int kMaxArgs = 24;
+  alignas(16) unsigned char slot[kMaxArgs][16];
+  void *ptr[kMaxArgs];
   void **args() {
     for (int i = 0; i < nargs; ++i) ptr[i] = slot[i];
     return ptr;
@@ -93,6 +94,7 @@ void put_args(Launch &L, A a, R... rest) {
 }
 template <typename... Args>
 Launch make_launch(const void *func, dim3 grid, dim3 block, int slab, Args... args) {
+  static_assert(sizeof...(Args) <= Launch::kMaxArgs, "too many kernel arguments for Launch");
   Launch L;
   L.func = func;
   L.grid = grid;

@@ -21,7 +21,8 @@ import numpy as np
 from . import _lib
 from .workloads import DeviceSolver, Times, _dims_scalars, _kind_of_state, _norm_dtype, _NP_DTYPE
 
-__all__ = ["slab_bounds", "halo_window", "exchange_plan", "unique_id", "DistributedSolver"]
+__all__ = ["slab_bounds", "halo_window", "exchange_plan", "unique_id", "seeded_window",
+           "DistributedSolver"]
 
 
 def slab_bounds(rows: int, world: int, rank: int) -> tuple[int, int]:
@@ -53,6 +54,28 @@ def exchange_plan(rows: int, world: int, rank: int) -> list[tuple[str, int, int,
     if rank < world - 1:
         plan += [("send", rank + 1, n), ("recv", rank + 1, n + 1)]
     return plan
+
+
+def seeded_window(shape, rank: int, world: int, seed: int = 20240817):
+    """This rank's (temperature window with halo rows, power rows) of the reference's seeded input.
+
+    The reference builds T = rng.random(shape) then P = rng.random(shape) * 1e-3 from one
+    default_rng(seed) stream (cli.py:173,182,192). PCG64 draws one 64-bit word per double, so a
+    rank advances the bit generator to its first row and draws only its window — the values are
+    identical to slicing the global arrays, without any rank materialising them.
+    """
+    shape = tuple(int(x) for x in shape)
+    rows = shape[0]
+    plane = int(np.prod(shape[1:]))
+    lo, hi = slab_bounds(rows, world, rank)
+    wlo, whi = halo_window(rows, world, rank)
+    bg = np.random.PCG64(seed)
+    bg.advance(wlo * plane)
+    t = np.random.Generator(bg).random((whi - wlo,) + shape[1:])
+    bg = np.random.PCG64(seed)
+    bg.advance(rows * plane + lo * plane)
+    p = np.random.Generator(bg).random((hi - lo,) + shape[1:]) * 1e-3
+    return t, p
 
 
 def unique_id() -> bytes:
@@ -102,6 +125,22 @@ class DistributedSolver(DeviceSolver):
         self.batch_size = 0
         if upload:
             self.upload(state)
+
+    @classmethod
+    def from_seed(cls, shape, k: float, dtype, rank: int, world: int, device: int,
+                  uid: bytes | None, seed: int = 20240817) -> "DistributedSolver":
+        """Build this rank's slab of the reference generator's grid (cli.py:183-192) directly."""
+
+        class _Shape:  # the global state's metadata only; the arrays come from seeded_window
+            def __init__(self, shape, k):
+                self.temperature = np.lib.stride_tricks.as_strided(np.zeros(1), shape, [0] * len(shape))
+                self.power = self.temperature
+                self.diffusion_coefficient = float(k)
+
+        solver = cls(_Shape(shape, k), dtype, rank, world, device, uid, upload=False)
+        t, p = seeded_window(shape, rank, world, seed)
+        solver.upload([t, p])
+        return solver
 
     def host_arrays(self, state):
         t = np.ascontiguousarray(state.temperature[self.wlo:self.whi], dtype=self.np_dtype)

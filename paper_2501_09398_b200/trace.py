@@ -57,6 +57,13 @@ def _arm(solver, capacity: int) -> None:
     _lib.check(_lib.lib().ib_trace_enable(solver.ctx, int(capacity)))
 
 
+def _arm_warm(solver, capacity: int) -> None:
+    """Arm, absorb CUPTI's one-off first-launch setup with a throwaway kernel, re-arm (clears)."""
+    _arm(solver, capacity)
+    solver.run_stream(1)
+    _arm(solver, capacity)
+
+
 def _collect(solver, capacity: int):
     L = _lib.lib()
     buf = np.zeros(2 * capacity, dtype=np.int64)
@@ -75,7 +82,7 @@ def capture_graph(solver, batch_size: int, num_batches: int, pdl: bool = False) 
     """Build a batch_size-iteration graph and replay it num_batches times, traced."""
     kpi = solver.kernels_per_iteration
     cap = batch_size * num_batches * kpi
-    _arm(solver, cap)
+    _arm_warm(solver, cap)
     solver.build_graph(batch_size, pdl=pdl)
     solver.run_graph(num_batches)
     solver.destroy_graph()
@@ -89,7 +96,7 @@ def capture_stream(solver, iterations: int, pdl: bool = False) -> RealTrace:
     """Listing 1 (one launch per kernel), traced; each kernel is its own 'batch'."""
     kpi = solver.kernels_per_iteration
     cap = iterations * kpi
-    _arm(solver, cap)
+    _arm_warm(solver, cap)
     solver.run_stream(iterations, pdl=pdl)
     kern, host, n = _collect(solver, cap)
     if n != cap:

@@ -134,3 +134,18 @@ def test_exchange_plan_pairs_every_send_with_a_recv():
         match = [x for x in recvs if x[0] == peer and x[1] == r]
         assert len(match) == 1
         assert (row == 1 and match[0][2] == match[0][3] + 1) or (row == n and match[0][2] == 0)
+
+
+@pytest.mark.parametrize("shape,world", [((11, 4, 3), 3), ((8, 5), 2), ((2048, 4), 8)])
+def test_seeded_window_equals_slicing_the_reference_generator(shape, world):
+    from paper_2501_09398_b200.cli import WORKLOAD_SEED
+    from paper_2501_09398_b200.distributed import seeded_window
+
+    rng = np.random.default_rng(WORKLOAD_SEED)
+    T = rng.random(shape)
+    P = rng.random(shape) * 1e-3
+    for rank in range(world):
+        t, p = seeded_window(shape, rank, world)
+        lo, hi = slab_bounds(shape[0], world, rank)
+        wlo, whi = halo_window(shape[0], world, rank)
+        assert np.array_equal(t, T[wlo:whi]) and np.array_equal(p, P[lo:hi])
