@@ -713,168 +713,202 @@ __global__ void __launch_bounds__(256)
 }
 
 // ================================================================================================
-// FDTD, fused leapfrog: one kernel per iteration (H half-step then E half-step), fields double
-// buffered (old -> new), so every field is read once and written once per iteration: 48 B/cell in
-// binary32 instead of the two-kernel 72.4 B/cell. Same arithmetic, bit for bit.
-// A CTA owns an (8 y x 32 z) tile of the unified lattice and marches a chunk of x-planes. Per
-// plane it computes H_new on the tile plus a one-cell low halo (y-1 row, z-1 column) into shared
-// memory — the E update needs H_new at y-1 / z-1 — from E_old planes x and x+1 kept in a 2-plane
-// shared-memory ring (10 x 34 cells per component), then updates E on the tile; H_new at x-1 is
-// carried in registers. The next plane's E and H_old loads are issued into registers before the
-// current plane's arithmetic, so they are in flight while it computes. A chunk starting at x0 > 0
-// first recomputes H_new(x0-1) (no writes) to seed the carry.
+// FDTD, fused leapfrog: ONE kernel per iteration (H half-step then E half-step), fields double
+// buffered (parity p -> p^1), so every field is read once and written once per iteration:
+// 48 B/cell in binary32 instead of the two-kernel 72.4 B/cell. Same arithmetic, bit for bit.
+//
+// Device layout (padded lattice): all six fields live on one (nx+1) x (ny+1) x P lattice, P =
+// nz+1 rounded up to 16 bytes, field f at base + f*FS. Lattice cells outside a field's true extent
+// hold 0 (allocation memset; the kernel writes masked zeros there) and never feed a result. Every
+// (plane, y-row range) of a field is one contiguous 16-byte aligned span: one cp.async.bulk.
+//
+// Work: a unit is (y-tile of h <= TJ rows, x-plane); the ny+1 rows are split evenly over the
+// tiles, so the host can make tiles x chunks fill the resident slots exactly. Default (chunks > 0): CTA = (tile, x-chunk) with
+// the same chunk bounds for every tile, so y-neighbour tiles stream the same planes at the same
+// time and the halo rows they share are served from L2, not re-read from HBM. chunks == 0: the
+// tile-major unit list is split evenly over the grid (a CTA may run across tiles).
+// A CTA marches its planes in x. One elected thread keeps NS planes of E_old rows [j0-1, j0+TJ]
+// and H_old rows [j0-1, j0+TJ-1] in flight into an NS-stage shared-memory ring (cp.async.bulk,
+// completion on per-stage mbarriers). Thread (r, g) owns lattice row j0-1+r and the V-element
+// 16-byte group g of the z row (V = 4 floats / 2 doubles):
+//   phase H: H_new(i) of its group from E_old(i), E_old(i+1) (next stage) and H_old(i); the
+//            result stays in registers, overwrites H_old(i) in the ring and (owned rows) goes to
+//            global with 16-byte stores;
+//   -- one CTA barrier --
+//   phase E (rows r >= 1): E_new(i) from E_old(i) and H_new(i) (own registers; row j-1 and
+//            column k-1 from the ring) and H_new(i-1) hy/hz carried in registers.
+// The barrier of plane t also proves every thread is done with plane t-1's stage, which is then
+// refilled. Masks are branch-free selects; a run starting at x0 > 0 first recomputes H_new(x0-1)
+// without writing, to seed the carry.
 // ================================================================================================
-namespace fused {
-constexpr int TK = 32, TJ = 8;              // owned tile (z fastest)
-constexpr int EJ = TJ + 2, EK = TK + 2;     // E tile: y in [j0-1, j0+8], z in [k0-1, k0+32]
-constexpr int RJ = TJ + 1, RK = TK + 1;     // H region: y in [j0-1, j0+8), z in [k0-1, k0+32)
-constexpr int ECELLS = EJ * EK;             // 340
-constexpr int RCELLS = RJ * RK;             // 297
-constexpr int EPF = (3 * ECELLS + 255) / 256;  // E loads per thread per plane (4)
-}  // namespace fused
+constexpr int kLfMaxThreads = 384;  // (TJ+1) x groups-per-row threads, rounded up to warps
 
-template <typename T, bool UNIT_D>
-__global__ void __launch_bounds__(256)
-    k_fdtd_fused(const T *__restrict__ ex0, const T *__restrict__ ey0, const T *__restrict__ ez0,
-                 const T *__restrict__ hx0, const T *__restrict__ hy0, const T *__restrict__ hz0,
-                 T *__restrict__ ex1, T *__restrict__ ey1, T *__restrict__ ez1, T *__restrict__ hx1,
-                 T *__restrict__ hy1, T *__restrict__ hz1, int nx, int ny, int nz, int planes_per_cta,
-                 T c_h, T c_e, T d) {
-  using namespace fused;
-  __shared__ T sE[2][3][EJ][EK];  // E_old planes (ring of 2): [buf][ex,ey,ez][y][z]
-  __shared__ T sH[3][RJ][RK];     // H_new of the current plane on the region: [hx,hy,hz]
+template <typename T, bool UNIT_D, int TJ>
+__global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
+    k_fdtd_lf(const T *__restrict__ src, T *__restrict__ dst, int nx, int ny, int nz, int P,
+              int64_t FS, int tiles, int chunks, int nstages, T c_h, T c_e, T d) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int V = 16 / sizeof(T);
+  constexpr int ER = TJ + 2, HR = TJ + 1;  // E rows / H rows per stage
   pdl_trigger();
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TK + tx;
-  const int k0 = blockIdx.x * TK, j0 = blockIdx.y * TJ;
-  const int i0 = blockIdx.z * planes_per_cta;
-  const int i1 = min(nx + 1, i0 + planes_per_cta);
-  const int ib = i0 > 0 ? i0 - 1 : 0;
-  const int ny1 = ny + 1, nz1 = nz + 1;
-  pdl_wait();
-
-  // E tile element e (0..3*ECELLS) -> (component, y, z); returns the global offset or -1
-  auto e_off = [&](int e, int i, int &c, int &ej, int &ek) -> int64_t {
-    c = e / ECELLS;
-    const int r = e - c * ECELLS;
-    ej = r / EK;
-    ek = r - ej * EK;
-    const int j = j0 - 1 + ej, k = k0 - 1 + ek;
-    if (j < 0 || k < 0) return -1;
-    if (c == 0) return (i < nx && j <= ny && k <= nz) ? ((int64_t)i * ny1 + j) * nz1 + k : -1;
-    if (c == 1) return (i <= nx && j < ny && k <= nz) ? ((int64_t)i * ny + j) * nz1 + k : -1;
-    return (i <= nx && j <= ny && k < nz) ? ((int64_t)i * ny1 + j) * nz + k : -1;
-  };
-  auto e_load = [&](int i, T (&v)[EPF]) {
+  T *ring = reinterpret_cast<T *>(smem_raw);
+  const int stage = 3 * (ER + HR) * P;  // elements per stage
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ring + (size_t)nstages * stage);
+  const int tid = threadIdx.x;
+  const int G = P / V;
+  const int r = tid / G, k0 = (tid - r * G) * V;
+  const int ny1 = ny + 1, nxp = nx + 1;
+  int64_t u_begin, u_end;
+  if (chunks > 0) {  // lockstep: CTA = (tile, x-chunk), equal chunk bounds for every tile
+    const int tile = blockIdx.x / chunks, ch = blockIdx.x - tile * chunks;
+    u_begin = (int64_t)tile * nxp + (int64_t)nxp * ch / chunks;
+    u_end = (int64_t)tile * nxp + (int64_t)nxp * (ch + 1) / chunks;
+  } else {  // even split of the tile-major unit list over the grid
+    const int64_t W = (int64_t)tiles * nxp;
+    u_begin = W * blockIdx.x / gridDim.x;
+    u_end = W * (blockIdx.x + 1) / gridDim.x;
+  }
+  // per-element z masks
+  bool klt[V], kle[V], kin[V];
 #pragma unroll
-    for (int q = 0; q < EPF; ++q) {
-      const int e = tid + q * 256;
-      int c, ej, ek;
-      const int64_t o = (e < 3 * ECELLS && i <= nx) ? e_off(e, i, c, ej, ek) : -1;
-      v[q] = o < 0 ? T(0) : (c == 0 ? ex0[o] : c == 1 ? ey0[o] : ez0[o]);
-    }
-  };
-  auto e_store = [&](int buf, const T (&v)[EPF]) {
-#pragma unroll
-    for (int q = 0; q < EPF; ++q) {
-      const int e = tid + q * 256;
-      if (e < 3 * ECELLS) {
-        const int c = e / ECELLS, r = e - c * ECELLS;
-        sE[buf][c][r / EK][r % EK] = v[q];
-      }
-    }
-  };
-  // the region points this thread computes H for: e = tid and e = tid + 256 (< RCELLS)
-  auto h_load = [&](int i, T (&h)[2][3]) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int e = tid + q * 256;
-      const int rj = e / RK, rk = e - (e / RK) * RK;
-      const int j = j0 - 1 + rj, k = k0 - 1 + rk;
-      const bool in = e < RCELLS && j >= 0 && k >= 0;
-      h[q][0] = (in && i <= nx && j < ny && k < nz) ? hx0[((int64_t)i * ny + j) * nz + k] : T(0);
-      h[q][1] = (in && i < nx && j <= ny && k < nz) ? hy0[((int64_t)i * ny1 + j) * nz + k] : T(0);
-      h[q][2] = (in && i < nx && j < ny && k <= nz) ? hz0[((int64_t)i * ny + j) * nz1 + k] : T(0);
-    }
-  };
-
-  T ev[EPF], hv[2][3];
-  e_load(ib, ev);
-  e_store(0, ev);
-  e_load(ib + 1, ev);
-  e_store(1, ev);
-  h_load(ib, hv);
+  for (int e = 0; e < V; ++e) {
+    const int k = k0 + e;
+    klt[e] = k < nz;
+    kle[e] = k <= nz;
+    kin[e] = k >= 1 && k < nz;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < nstages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
-
-  const int j = j0 + ty, k = k0 + tx;  // this thread's own lattice point
-  const bool mine = j <= ny && k <= nz;
-  T hy_prev = T(0), hz_prev = T(0);
-  int cur = 0;
-  for (int i = ib; i < i1; ++i) {
-    const bool write = i >= i0;
-    // prefetch E_old(i+2) and H_old(i+1) while this plane computes
-    T evn[EPF], hvn[2][3];
-    e_load(i + 2, evn);
-    h_load(i + 1, hvn);
-    // ---- H_new(i) on the region -------------------------------------------------------------
-    const int nxt = cur ^ 1;
+  pdl_wait();  // the previous iteration's writes are visible from here on
+  uint32_t g_base = 0;  // stage uses so far (mbarrier phase bookkeeping across runs)
+  for (int64_t u = u_begin; u < u_end;) {
+    const int tile = (int)(u / nxp);
+    const int i0 = (int)(u - (int64_t)tile * nxp);
+    const int i1 = (int)min((int64_t)nxp, (int64_t)i0 + (u_end - u));
+    u += i1 - i0;
+    // tile rows [j0, j0 + h), h <= TJ: the (ny+1) rows split evenly over `tiles` tiles
+    const int j0 = (int)((int64_t)(ny + 1) * tile / tiles);
+    const int h = (int)((int64_t)(ny + 1) * (tile + 1) / tiles) - j0;
+    const int ib = i0 > 0 ? i0 - 1 : 0;
+    const int nload = min(i1, nx) - ib + 1;  // stages: planes ib .. min(i1, nx)
+    const int elo = max(j0 - 1, 0), ehi = min(j0 + h, ny), hhi = min(j0 + h - 1, ny);
+    const uint32_t ebytes = (uint32_t)((ehi - elo + 1) * P * sizeof(T));
+    const uint32_t hbytes = (uint32_t)((hhi - elo + 1) * P * sizeof(T));
+    const int erow0 = elo - (j0 - 1);  // ring row of lattice row elo
+    auto issue = [&](int t) {
+      const int s = (int)((g_base + t) % nstages);
+      const int p = ib + t;
+      const bool h = p < i1;
+      T *st = ring + (size_t)s * stage;
+      mbar_expect_tx(&bar[s], 3 * ebytes + (h ? 3 * hbytes : 0u));
+      const int64_t row = (int64_t)p * ny1 + elo;
+      for (int c = 0; c < 3; ++c)
+        bulk_g2s(st + (c * ER + erow0) * P, src + c * FS + row * P, ebytes, &bar[s]);
+      if (h)
+        for (int c = 0; c < 3; ++c)
+          bulk_g2s(st + 3 * ER * P + (c * HR + erow0) * P, src + (3 + c) * FS + row * P, hbytes, &bar[s]);
+    };
+    __syncthreads();  // every thread is done with the previous run's stages
+    if (tid == 0) {
+      fence_proxy_async();
+      for (int t = 0; t < min(nstages, nload); ++t) issue(t);
+    }
+    const int jj = j0 - 1 + r;  // this thread's lattice row
+    const bool row_ok = r <= h && jj >= 0 && jj <= ny;
+    const bool jlt = jj < ny, jin = jj >= 1 && jj < ny;
+    T hy_prev[V], hz_prev[V];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int e = tid + q * 256;
-      if (e >= RCELLS) continue;
-      const int rj = e / RK, rk = e - (e / RK) * RK;
-      const int jj = j0 - 1 + rj, kk = k0 - 1 + rk;
-      T hxn = T(0), hyn = T(0), hzn = T(0);
-      if (jj >= 0 && kk >= 0) {
-        if (jj < ny && kk < nz)  // hx: ey(z+1)-ey, ez(y+1)-ez
-          hxn = curl2<T, UNIT_D>(hv[q][0], c_h, sE[cur][1][rj][rk + 1], sE[cur][1][rj][rk],
-                                 sE[cur][2][rj + 1][rk], sE[cur][2][rj][rk], d);
-        if (i < nx && jj <= ny && kk < nz)  // hy: ez(x+1)-ez, ex(z+1)-ex
-          hyn = curl2<T, UNIT_D>(hv[q][1], c_h, sE[nxt][2][rj][rk], sE[cur][2][rj][rk],
-                                 sE[cur][0][rj][rk + 1], sE[cur][0][rj][rk], d);
-        if (i < nx && jj < ny && kk <= nz)  // hz: ex(y+1)-ex, ey(x+1)-ey
-          hzn = curl2<T, UNIT_D>(hv[q][2], c_h, sE[cur][0][rj + 1][rk], sE[cur][0][rj][rk],
-                                 sE[nxt][1][rj][rk], sE[cur][1][rj][rk], d);
-        if (write && rj >= 1 && rk >= 1) {  // owned points only
-          if (jj < ny && kk < nz) hx1[((int64_t)i * ny + jj) * nz + kk] = hxn;
-          if (i < nx && jj <= ny && kk < nz) hy1[((int64_t)i * ny1 + jj) * nz + kk] = hyn;
-          if (i < nx && jj < ny && kk <= nz) hz1[((int64_t)i * ny + jj) * nz1 + kk] = hzn;
+    for (int e = 0; e < V; ++e) hy_prev[e] = hz_prev[e] = T(0);
+    for (int i = ib; i < i1; ++i) {
+      const int t = i - ib;
+      const bool write = i >= i0;
+      const uint32_t gs = g_base + t;
+      if (t == 0) mbar_wait(&bar[gs % nstages], (gs / nstages) & 1);
+      if (t + 1 < nload) mbar_wait(&bar[(gs + 1) % nstages], ((gs + 1) / nstages) & 1);
+      const T *Ec = ring + (size_t)(gs % nstages) * stage + r * P + k0;  // E_old(i), my row/group
+      const T *En = ring + (size_t)((gs + 1) % nstages) * stage + r * P + k0;  // E_old(i+1)
+      T *Hr = ring + (size_t)(gs % nstages) * stage + 3 * ER * P + r * P + k0;  // H(i), my row/group
+      const bool ilt = i < nx, iin = i >= 1 && i < nx;
+      T exr[V], eyr[V], ezr[V], hx[V], hy[V], hz[V];
+      // ---- phase H --------------------------------------------------------------------------
+      if (row_ok) {
+        T exd[V], ezd[V], eyn[V], ezn[V];
+        ld16<T>(exr, Ec);
+        ld16<T>(eyr, Ec + ER * P);
+        ld16<T>(ezr, Ec + 2 * ER * P);
+        ld16<T>(exd, Ec + P);               // row j+1
+        ld16<T>(ezd, Ec + 2 * ER * P + P);
+        ld16<T>(hx, Hr);
+        ld16<T>(hy, Hr + HR * P);
+        ld16<T>(hz, Hr + 2 * HR * P);
+        const T exk = Ec[V], eyk = Ec[ER * P + V];  // column k0+V
+        if (ilt) {
+          ld16<T>(eyn, En + ER * P);
+          ld16<T>(ezn, En + 2 * ER * P);
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) eyn[e] = ezn[e] = T(0);
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const T ey1 = e + 1 < V ? eyr[e + 1] : eyk;  // ey(k+1)
+          const T ex1 = e + 1 < V ? exr[e + 1] : exk;  // ex(k+1)
+          const T a = curl2<T, UNIT_D>(hx[e], c_h, ey1, eyr[e], ezd[e], ezr[e], d);     // ey(k+1)-ey, ez(j+1)-ez
+          const T b = curl2<T, UNIT_D>(hy[e], c_h, ezn[e], ezr[e], ex1, exr[e], d);     // ez(i+1)-ez, ex(k+1)-ex
+          const T c = curl2<T, UNIT_D>(hz[e], c_h, exd[e], exr[e], eyn[e], eyr[e], d);  // ex(j+1)-ex, ey(i+1)-ey
+          hx[e] = (jlt && klt[e]) ? a : T(0);
+          hy[e] = (ilt && klt[e]) ? b : T(0);
+          hz[e] = (ilt && jlt && kle[e]) ? c : T(0);
+        }
+        st16<T>(Hr, hx);
+        st16<T>(Hr + HR * P, hy);
+        st16<T>(Hr + 2 * HR * P, hz);
+        if (write && r >= 1) {
+          T *o = dst + ((int64_t)i * ny1 + jj) * P + k0;
+          st16<T>(o + 3 * FS, hx);
+          st16<T>(o + 4 * FS, hy);
+          st16<T>(o + 5 * FS, hz);
         }
       }
-      sH[0][rj][rk] = hxn;
-      sH[1][rj][rk] = hyn;
-      sH[2][rj][rk] = hzn;
-    }
-    __syncthreads();
-    // ---- E_new(i) on the owned tile ---------------------------------------------------------
-    const int rj = ty + 1, rk = tx + 1;
-    if (mine && write) {
-      const bool iin = i >= 1 && i < nx, jin = j >= 1 && j < ny, kin = k >= 1 && k < nz;
-      if (i < nx)  // ex: hz(y)-hz(y-1), hy(z)-hy(z-1); walls y in {0,ny}, z in {0,nz}
-        ex1[((int64_t)i * ny1 + j) * nz1 + k] =
-            (jin && kin) ? curl2<T, UNIT_D>(sE[cur][0][rj][rk], c_e, sH[2][rj][rk], sH[2][rj - 1][rk],
-                                            sH[1][rj][rk], sH[1][rj][rk - 1], d)
-                         : T(0);
-      if (j < ny)  // ey: hx(z)-hx(z-1), hz(x)-hz(x-1); walls x in {0,nx}, z in {0,nz}
-        ey1[((int64_t)i * ny + j) * nz1 + k] =
-            (iin && kin) ? curl2<T, UNIT_D>(sE[cur][1][rj][rk], c_e, sH[0][rj][rk], sH[0][rj][rk - 1],
-                                            sH[2][rj][rk], hz_prev, d)
-                         : T(0);
-      if (k < nz)  // ez: hy(x)-hy(x-1), hx(y)-hx(y-1); walls x in {0,nx}, y in {0,ny}
-        ez1[((int64_t)i * ny1 + j) * nz + k] =
-            (iin && jin) ? curl2<T, UNIT_D>(sE[cur][2][rj][rk], c_e, sH[1][rj][rk], hy_prev,
-                                            sH[0][rj][rk], sH[0][rj - 1][rk], d)
-                         : T(0);
-    }
-    hy_prev = sH[1][rj][rk];
-    hz_prev = sH[2][rj][rk];
-    __syncthreads();  // sE[cur] and sH are free
-    e_store(cur, evn);  // E_old(i+2) replaces E_old(i)
+      __syncthreads();  // H_new(i) complete in the ring; plane t-1's stage is free
+      if (tid == 0 && t >= 1 && t - 1 + nstages < nload) {
+        fence_proxy_async();
+        issue(t - 1 + nstages);
+      }
+      // ---- phase E (owned rows) ---------------------------------------------------------------
+      if (row_ok && r >= 1) {
+        if (write) {
+          T hzu[V], hxu[V], ex[V], ey[V], ez[V];
+          ld16<T>(hxu, Hr - P);               // row j-1
+          ld16<T>(hzu, Hr + 2 * HR * P - P);
+          const T hxm = Hr[-1], hym = Hr[HR * P - 1];  // column k0-1
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+          for (int e = 0; e < V; ++e) {
+            const T hy0 = e > 0 ? hy[e - 1] : hym;  // hy(k-1)
+            const T hx0 = e > 0 ? hx[e - 1] : hxm;  // hx(k-1)
+            const T a = curl2<T, UNIT_D>(exr[e], c_e, hz[e], hzu[e], hy[e], hy0, d);         // hz(j)-hz(j-1), hy(k)-hy(k-1)
+            const T b = curl2<T, UNIT_D>(eyr[e], c_e, hx[e], hx0, hz[e], hz_prev[e], d);     // hx(k)-hx(k-1), hz(i)-hz(i-1)
+            const T c = curl2<T, UNIT_D>(ezr[e], c_e, hy[e], hy_prev[e], hx[e], hxu[e], d);  // hy(i)-hy(i-1), hx(j)-hx(j-1)
+            ex[e] = (ilt && jin && kin[e]) ? a : T(0);  // walls y in {0,ny}, z in {0,nz}
+            ey[e] = (jlt && iin && kin[e]) ? b : T(0);  // walls x in {0,nx}, z in {0,nz}
+            ez[e] = (klt[e] && iin && jin) ? c : T(0);  // walls x in {0,nx}, y in {0,ny}
+          }
+          T *o = dst + ((int64_t)i * ny1 + jj) * P + k0;
+          st16<T>(o, ex);
+          st16<T>(o + FS, ey);
+          st16<T>(o + 2 * FS, ez);
+        }
 #pragma unroll
-      for (int c = 0; c < 3; ++c) hv[q][c] = hvn[q][c];
-    cur = nxt;
-    __syncthreads();
+        for (int e = 0; e < V; ++e) {
+          hy_prev[e] = hy[e];
+          hz_prev[e] = hz[e];
+        }
+      }
+    }
+    g_base += (uint32_t)nload;
   }
 }
 

@@ -232,6 +232,10 @@ struct ib_ctx {
   std::vector<Slab> slabs;
   void *field[6] = {};      // vector / fdtd device fields (single slab)
   void *field2[6] = {};     // fused fdtd: the second buffer of the ping-pong field pairs
+  // fused fdtd: the padded lattice (two parities), fields at lat[p] + f*lat_fs elements, rows of
+  // lat_pitch elements (nz+1 rounded up to 16 bytes); field/field2 point into it
+  void *lat[2] = {nullptr, nullptr};
+  int64_t lat_pitch = 0, lat_fs = 0;
   int64_t fshape[6][3] = {};
   int fndim[6] = {};
   int nfields = 0;
@@ -485,32 +489,98 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
                             d, unit));
 }
 
+// Fused leapfrog (k_fdtd_lf): TJ y-rows per tile, NS-stage bulk-copy ring. The largest TJ (and
+// then NS) whose ring lets two CTAs share an SM; the grid is one wave of resident CTAs and the
+// (tile, plane) units are split evenly over it. IB_FDTD_TJ / IB_FDTD_STAGES override.
+struct LfConfig {
+  int tj = 0, ns = 0;
+  size_t smem = 0;
+};
+inline size_t lf_smem(int tj, int ns, int64_t P, int es) {
+  return (size_t)ns * (size_t)(3 * (tj + 2) + 3 * (tj + 1)) * (size_t)P * es + (size_t)ns * 8;
+}
+inline int lf_threads(const ib_ctx *c, int tj) {  // one thread per (row, 16-byte group)
+  const int64_t groups = c->lat_pitch / (16 / c->esize);
+  return (int)(((tj + 1) * groups + 31) / 32 * 32);
+}
+inline LfConfig lf_config(const ib_ctx *c) {
+  // The kernel is bound by the bytes each SM keeps in flight, CTAs/SM x (NS-1) x stage bytes.
+  // Measured at 256^3 binary32 (us/iter): TJ=4/NS=6/1 per SM 130.7, TJ=4/NS=5 137.3,
+  // TJ=3/NS=4/2 per SM 138.5, TJ=3/NS=3/2 per SM 196, TJ=4/NS=3/2 per SM 171. So: 4-row tiles
+  // with the deepest ring one CTA per SM holds (<= 6 stages), then 2 per SM, then smaller tiles.
+  const int64_t P = c->lat_pitch;
+  const int es = c->esize;
+  const size_t cap = 227 * 1024, half = 113 * 1024;
+  LfConfig cfg;
+  const int64_t ftj = env_int("IB_FDTD_TJ", 0), fns = env_int("IB_FDTD_STAGES", 0);
+  const struct { int tj; bool two; } order[] = {{4, false}, {3, true}, {4, true}, {2, true},
+                                                 {3, false}, {2, false}, {1, true}, {1, false}};
+  for (auto o : order) {
+    if (ftj > 0 && o.tj != ftj) continue;
+    if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
+    for (int ns = 3; ns <= 8; ++ns) {
+      if (fns > 0 && ns != fns) continue;
+      const size_t sm = lf_smem(o.tj, ns, P, es);
+      if (sm <= (o.two ? half : cap) && (fns > 0 || ns <= 6)) cfg = {o.tj, ns, sm};
+    }
+    if (cfg.tj && (cfg.ns >= 4 || fns > 0 || ftj > 0)) break;
+    if (cfg.tj && o.tj == 1) break;
+    if (cfg.tj && cfg.ns < 4) cfg = LfConfig{};  // too shallow: try the next shape
+  }
+  if (!cfg.tj) {  // nothing deep enough: take any shape that fits
+    for (auto o : order) {
+      if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
+      const size_t sm = lf_smem(o.tj, 3, P, es);
+      if (sm <= cap) { cfg = {o.tj, 3, sm}; break; }
+    }
+  }
+  return cfg;
+}
+
+template <typename T, bool U>
+const void *lf_fn(int tj) {
+  switch (tj) {
+    case 1: return (const void *)ib::k_fdtd_lf<T, U, 1>;
+    case 2: return (const void *)ib::k_fdtd_lf<T, U, 2>;
+    case 3: return (const void *)ib::k_fdtd_lf<T, U, 3>;
+    default: return (const void *)ib::k_fdtd_lf<T, U, 4>;
+  }
+}
+
 template <typename T>
 void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
   const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
   const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
   const bool unit = c->scalars[0] == 1.0;
-  const void *fn = unit ? (const void *)ib::k_fdtd_fused<T, true> : (const void *)ib::k_fdtd_fused<T, false>;
-  const int64_t tiles = (int64_t)((nz + 1 + 31) / 32) * ((ny + 1 + 7) / 8);
+  const LfConfig cfg = lf_config(c);
+  const void *fn = unit ? lf_fn<T, true>(cfg.tj) : lf_fn<T, false>(cfg.tj);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+  const int threads = lf_threads(c, cfg.tj);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, cfg.smem);
+  // Lockstep (tile, x-chunk) grid: as many x-chunks as the resident slots hold whole columns of
+  // TJ-row tiles (256^3, TJ=4, 148 slots: 65 tiles x 2 chunks). Filling the spare slots with
+  // shorter tiles (74 tiles of 3-4 rows x 2) measured slower (137 vs 131 us): more halo rows.
+  // IB_FDTD_TILES (uneven rows, h <= TJ), IB_FDTD_CHUNKS, IB_FDTD_CTAS (even split) override.
   const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
-  int64_t ppc = env_int("IB_FDTD_PPC", 0);
-  if (ppc <= 0) {  // x-chunks so the grid is about one wave of resident CTAs
-    const int64_t chunks = std::max<int64_t>(1, slots / tiles);
-    ppc = (nx + 1 + chunks - 1) / chunks;
+  const int64_t min_tiles = (ny + 1 + cfg.tj - 1) / cfg.tj;
+  int64_t tiles = min_tiles;
+  if (env_int("IB_FDTD_TILES", 0) >= min_tiles) tiles = std::min<int64_t>(ny + 1, env_int("IB_FDTD_TILES", 0));
+  int64_t chunks = env_int("IB_FDTD_CHUNKS", 0);
+  if (chunks <= 0) chunks = std::max<int64_t>(1, slots / tiles);
+  chunks = std::min<int64_t>(chunks, nx + 1);  // every chunk non-empty
+  int64_t ctas = env_int("IB_FDTD_CTAS", 0);
+  if (ctas <= 0) {
+    ctas = tiles * chunks;  // one CTA per (tile, chunk): the kernel maps blockIdx.x to both
+  } else {
+    chunks = 0;  // even split of the tile-major unit list over `ctas` CTAs
+    ctas = std::max<int64_t>(1, std::min(ctas, tiles * (nx + 1)));
   }
-  ppc = std::max<int64_t>(1, std::min<int64_t>(ppc, nx + 1));
-  dim3 block(32, 8);
-  dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)((nx + 1 + ppc - 1) / ppc));
-  T *a[6], *b[6];
-  for (int f = 0; f < 6; ++f) {
-    a[f] = (T *)c->fieldp(f, parity);
-    b[f] = (T *)c->fieldp(f, parity ^ 1);
-  }
-  out.push_back(make_launch(fn, grid, block, 0, (const T *)a[0], (const T *)a[1], (const T *)a[2],
-                            (const T *)a[3], (const T *)a[4], (const T *)a[5], b[0], b[1], b[2], b[3],
-                            b[4], b[5], nx, ny, nz, (int)ppc, ch, ce, d));
+  Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), 0, (const T *)c->lat[parity],
+                         (T *)c->lat[parity ^ 1], nx, ny, nz, (int)c->lat_pitch, c->lat_fs, (int)tiles,
+                         (int)chunks, cfg.ns, ch, ce, d);
+  L.smem = cfg.smem;
+  out.push_back(L);
 }
 
 void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
@@ -873,9 +943,14 @@ void ib_destroy(ib_ctx *c) {
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   if (!c->slabs.empty()) cudaSetDevice(c->slabs[0].device);
-  for (int f = 0; f < 6; ++f) {
-    if (c->field[f]) cudaFree(c->field[f]);
-    if (c->field2[f]) cudaFree(c->field2[f]);
+  if (c->lat[0] || c->lat[1]) {
+    for (int p = 0; p < 2; ++p)
+      if (c->lat[p]) cudaFree(c->lat[p]);
+  } else {
+    for (int f = 0; f < 6; ++f) {
+      if (c->field[f]) cudaFree(c->field[f]);
+      if (c->field2[f]) cudaFree(c->field2[f]);
+    }
   }
   if (c->d_counter) cudaFree(c->d_counter);
   if (c->tracing) {
@@ -949,15 +1024,27 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
       IB_CUDA(cudaMemset(s.power, 0, (size_t)(s.rows() * plane * es)));
     }
     IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  } else if (c->solver == IB_SOLVER_FDTD_FUSED) {
+    const int64_t nx = c->dims[0], ny = c->dims[1], nz = c->dims[2];
+    const int64_t v = 16 / es;
+    c->lat_pitch = (nz + 1 + v - 1) / v * v;
+    c->lat_fs = (nx + 1) * (ny + 1) * c->lat_pitch;
+    if (lf_config(c).tj == 0)
+      return fail(IB_EINVAL, "fused fdtd: the z rows are too long for one CTA (threads or shared-memory ring); use the two-kernel solver");
+    const size_t b = (size_t)(6 * c->lat_fs * es);
+    for (int p = 0; p < 2; ++p) {
+      IB_CUDA(cudaMalloc(&c->lat[p], b));
+      IB_CUDA(cudaMemset(c->lat[p], 0, b));
+    }
+    for (int f = 0; f < 6; ++f) {
+      c->field[f] = (char *)c->lat[0] + (size_t)(f * c->lat_fs * es);
+      c->field2[f] = (char *)c->lat[1] + (size_t)(f * c->lat_fs * es);
+    }
   } else {
     for (int f = 0; f < c->nfields; ++f) {
       const size_t b = (size_t)(numel(c->fshape[f], c->fndim[f]) * es);
       IB_CUDA(cudaMalloc(&c->field[f], b));
       IB_CUDA(cudaMemset(c->field[f], 0, b));
-      if (c->solver == IB_SOLVER_FDTD_FUSED) {
-        IB_CUDA(cudaMalloc(&c->field2[f], b));
-        IB_CUDA(cudaMemset(c->field2[f], 0, b));
-      }
     }
   }
   IB_CUDA(cudaDeviceSynchronize());
@@ -1205,6 +1292,21 @@ static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
   if (c->hotspot()) return hotspot_copy(c, field, host, bytes, up);
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
   void *dev = c->fieldp(field, c->cur);
+  if (c->solver == IB_SOLVER_FDTD_FUSED) {  // C-order host array <-> padded lattice
+    const int64_t *sh = c->fshape[field];
+    const size_t es = (size_t)c->esize;
+    cudaMemcpy3DParms m = {};
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)sh[2] * es, (size_t)sh[2] * es, (size_t)sh[1]);
+    cudaPitchedPtr dp = make_cudaPitchedPtr(dev, (size_t)c->lat_pitch * es, (size_t)sh[2] * es,
+                                            (size_t)(c->dims[1] + 1));
+    m.srcPtr = up ? hp : dp;
+    m.dstPtr = up ? dp : hp;
+    m.extent = make_cudaExtent((size_t)sh[2] * es, (size_t)sh[1], (size_t)sh[0]);
+    m.kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    IB_CUDA(cudaMemcpy3DAsync(&m, c->stream()));
+    IB_CUDA(cudaStreamSynchronize(c->stream()));
+    return IB_OK;
+  }
   if (up)
     IB_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, c->stream()));
   else

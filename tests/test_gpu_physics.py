@@ -11,6 +11,7 @@ import math
 import numpy as np
 import pytest
 
+from oracle import cpu as ocpu
 from paper_2501_09398_b200 import workloads as wl
 
 pytestmark = pytest.mark.gpu
@@ -201,14 +202,20 @@ def test_real_trace_is_consistent(gpu, tmp_path):
     assert {"node_added", "graph_instantiated", "graph_uploaded", "graph_launched",
             "kernel_started", "kernel_ended", "batch_gap_started"} <= kinds
     p = tr.derive_parameters(g, st)
-    assert 0 < p["t_k"] < 1e-3 and p["t_i"] >= 0 and p["t_b"] >= 0 and p["k_c"] > 0
+    # CUPTI stamps kernel ends a few tens of ns late, so back-to-back graph kernels can show a
+    # slightly negative gap; the params file clamps at 0 (write_params)
+    assert 0 < p["t_k"] < 1e-3 and p["t_i"] > -0.5e-6 and p["t_b"] > -0.5e-6 and p["k_c"] > 0
     path = tmp_path / "g.csv"
     tr.write_trace_csv(g, path)
     lines = path.read_text().splitlines()
     assert lines[0] == "# schema=1" and lines[1] == "timestamp,kind,batch_index,kernel_index"
     # tracing off again: results unaffected, no records
-    ref = wl.state_checksum(wl.run_loop(wl.hotspot_program(), state, 10, dtype="f32"))
+    want = ocpu.hotspot(state.temperature, state.power, state.diffusion_coefficient, 10, np.float32)
+    ref = wl.run_loop(wl.hotspot_program(), state, 10, dtype="f32")
+    assert np.array_equal(np.asarray(ref.temperature, np.float32), want), "cached-context run_loop"
     s.upload(state)
     s.run_stream(10)
-    assert s.checksum() != 0 and wl.state_checksum(s.download(state)) == ref
+    got = s.download(state)
+    assert np.array_equal(np.asarray(got.temperature, np.float32), want), "traced solver after tracing"
+    assert s.checksum() != 0
     s.close()

@@ -115,14 +115,19 @@ def test_fdtd_non_unit_cell_size(gpu, env):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("ppc", [0, 1, 2, 3])
+@pytest.mark.parametrize("tj,ctas,chunks,tiles", [(0, 0, 0, 0), (1, 0, 0, 0), (2, 5, 0, 0), (3, 1, 0, 0),
+                                                  (4, 7, 0, 0), (4, 13, 0, 0), (2, 0, 3, 0), (4, 0, 1, 0),
+                                                  (1, 0, 4, 0), (4, 0, 2, 3), (3, 0, 1, 7), (4, 9, 0, 5)])
 @pytest.mark.parametrize("dims", FDTD_DIMS + [(40, 9, 70), (7, 17, 31)],
                          ids=["x".join(map(str, d)) for d in FDTD_DIMS + [(40, 9, 70), (7, 17, 31)]])
-def test_fdtd_fused_bitwise(gpu, env, dims, ppc, dtype):
-    """One kernel per iteration (H then E fused, double-buffered fields) == the oracle, bitwise."""
-    env(IB_FDTD_PPC=ppc)
+def test_fdtd_fused_bitwise(gpu, env, dims, tj, ctas, chunks, tiles, dtype):
+    """One kernel per iteration (H then E fused, double-buffered padded lattice) == the oracle,
+    bitwise, for every tile height, uneven row splits (tiles of h <= TJ rows), lockstep chunk
+    grids and CTA counts that split the (tile, plane) units into runs starting mid-tile (the
+    recomputed seed plane) and spanning several tiles."""
+    env(IB_FDTD_TJ=tj, IB_FDTD_CTAS=ctas, IB_FDTD_CHUNKS=chunks, IB_FDTD_TILES=tiles)
     base = wl.fdtd_cavity(*dims)
-    rng = np.random.default_rng(sum(dims) * 7 + ppc)
+    rng = np.random.default_rng(sum(dims) * 7 + tj + ctas + chunks + tiles)
     state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
                             base.cell_size, base.time_step)
     npd = np.float32 if dtype == "f32" else np.float64
@@ -136,3 +141,17 @@ def test_fdtd_fused_bitwise(gpu, env, dims, ppc, dtype):
     got = wl.run_loop(wl.fdtd_program(), state, 5, dtype=dtype, fuse=True)
     for g, w in zip(got.state_arrays(), want):
         assert np.array_equal(np.asarray(g, npd), w)
+
+
+@pytest.mark.parametrize("ctas", [0, 3])
+def test_fdtd_fused_non_unit_cell_size(gpu, env, ctas):
+    """Fused leapfrog with d != 1 (the division path) == the oracle, bitwise."""
+    env(IB_FDTD_CTAS=ctas)
+    w = wl.te101_cavity(6, 5, 7, cell_size=0.37)
+    dt = w.time_step
+    for dtype, npd in (("f64", np.float64), ("f32", np.float32)):
+        want = ocpu.fdtd(w.state_arrays(), 0.37, dt / wl.VACUUM_PERMEABILITY,
+                         dt / wl.VACUUM_PERMITTIVITY, 9, npd)
+        got = wl.run_loop(wl.fdtd_program(), w, 9, dtype=dtype, fuse=True)
+        for g, ww in zip(got.state_arrays(), want):
+            assert np.array_equal(np.asarray(g, npd), ww)

@@ -1,0 +1,31 @@
+"""FDTD 256^3 binary32: two-kernel vs fused leapfrog variants, device-timed (CUDA events)."""
+import os, sys, statistics
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2501_09398_b200 import cli, workloads as wl
+
+n = int(os.environ.get("N", "256"))
+st = cli.build_workload("fdtd", [n])
+variants = [("two-kernel", False, {})]
+variants.append(("fused default", True, {}))
+for tj, ns, chunks in ((4, 6, 1), (4, 6, 2), (4, 6, 3), (4, 5, 2), (3, 6, 2), (3, 4, 0), (2, 5, 0)):
+    variants.append((f"fused tj={tj} ns={ns} chunks={chunks}", True,
+                     {"IB_FDTD_TJ": tj, "IB_FDTD_STAGES": ns, "IB_FDTD_CHUNKS": chunks}))
+variants.append(("fused even-split ctas=296", True, {"IB_FDTD_CTAS": 296}))
+for name, fuse, env in variants:
+    for k in ("IB_FDTD_TJ", "IB_FDTD_STAGES", "IB_FDTD_CTAS", "IB_FDTD_CHUNKS", "IB_FDTD_TILES"):
+        os.environ.pop(k, None)
+    for k, v in env.items():
+        os.environ[k] = str(v)
+    try:
+        s = wl.DeviceSolver(st, "f32", fuse=fuse)
+    except Exception as e:
+        print(f"{name}: {e}", flush=True)
+        continue
+    s.run_batched(20, 5, pdl=True)
+    xs = []
+    for _ in range(3):
+        s.flush_l2()
+        xs.append(s.run_batched(20, 10, pdl=True).gpu_s / 200)
+    t = statistics.median(xs)
+    print(f"{name:36s} {1e6*t:8.1f} us/iter  {s.iteration_bytes/t/1e9:7.0f} GB/s", flush=True)
+    s.close()

@@ -16,10 +16,11 @@ ap.add_argument("--workload", required=True)
 ap.add_argument("--size", required=True)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--dtype", default="f32")
+ap.add_argument("--fuse", action="store_true", help="FDTD: the fused one-kernel leapfrog")
 ap.add_argument("--graph", type=int, default=0, help="also run a graph of this batch size")
 a = ap.parse_args()
 state = cli.build_workload(a.workload, [int(x) for x in a.size.split(",")])
-s = wl.DeviceSolver(state, a.dtype)
+s = wl.DeviceSolver(state, a.dtype, fuse=a.fuse)
 t = s.run_stream(a.iters)
 print(f"{a.workload} {a.size} {a.dtype}: {1e6 * t.gpu_s / a.iters:.2f} us/iter (stream, incl. profiler)")
 if a.graph:
