@@ -165,58 +165,68 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 }
 
 // ================================================================================================
-// Hotspot, vectorised one-row-per-thread variant for L2-resident grids (the launch-bound configs).
-// A thread owns V = 16/sizeof(T) consecutive cells of one plane row (one 16-byte load/store); all
-// of its loads are independent, so the whole grid's reads are in flight at once — no marching
-// chain. Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles
-// a y-row). grid = (ceil(M/V/256), rows).
+// Hotspot, vectorised variant for L2-resident grids (the launch-bound configs). A thread owns
+// V = 16/sizeof(T) consecutive cells of one plane row (one 16-byte load/store per row) and R
+// consecutive rows: the R+2 x-rows are loaded once, up front, all independent (L2->SM traffic for
+// T is (R+2)/R of the grid instead of 3x). Every edge clamp (np.pad "edge", workloads.py:177) is
+// an address clamp computed once per thread — the clamped neighbour of an edge cell is the cell
+// itself — so the per-row work is 5 loads, 1 store and the cell arithmetic, with 32-bit offsets
+// (the launch layer checks the slab buffer holds < 2^31 elements).
+// Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles a
+// y-row). grid = (ceil(M/V/256), ceil(rows/R)).
 // ================================================================================================
 template <typename T, bool D3, int R>
 __global__ void __launch_bounds__(256)
     k_hotspot_vec(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
                   int rows, int C, int L, T k, T loss, int has_top, int has_bot,
                   T *__restrict__ halo_up, T *__restrict__ halo_dn) {
-  // R consecutive rows per thread: the R+2 x-rows are loaded once (all loads independent and
-  // issued together), so L2->SM traffic for T drops from 3x to (R+2)/R x of the grid.
   constexpr int V = 16 / sizeof(T);
   pdl_trigger();
-  const int64_t M = (int64_t)C * L;
-  const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
+  const int M = C * L;
+  const int m = (blockIdx.x * blockDim.x + threadIdx.x) * V;
   const int i0 = blockIdx.y * R;
-  pdl_wait();
   if (m >= M) return;
   const int nr = min(R, rows - i0);
-  T x[R + 2][V], pw[R][V];
-  const T *s = src + m;
+  // neighbour offsets relative to the group's first cell, edge-clamped once
+  int oym, oyp, ozl, ozr;  // y-1 / y+1 group, z-1 / z+1 scalar (3-D); 2-D: y is the row axis
+  if (D3) {
+    const int l = m % L;
+    oym = m >= L ? -L : 0;
+    oyp = m + L < M ? L : 0;
+    ozl = l > 0 ? -1 : 0;
+    ozr = l + V < L ? V : V - 1;
+  } else {
+    oym = oyp = 0;
+    ozl = m > 0 ? -1 : 0;      // y-1 scalar
+    ozr = m + V < M ? V : V - 1;  // y+1 scalar
+  }
+  const int qlo = has_top ? -1 : 0, qhi = has_bot ? rows : rows - 1;
+  // the power field is never written by a step: load it before waiting on the previous kernel
+  // (with programmatic edges this overlaps the predecessor's tail)
+  T pw[R][V];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r < nr) ld16<T>(pw[r], power + (i0 + r) * M + m);
+  pdl_wait();
+  T x[R + 2][V];
 #pragma unroll
   for (int r = 0; r < R + 2; ++r) {
     int q = i0 - 1 + r;
-    if (q >= i0 + nr + 1) q = i0 + nr;                      // past the chunk: never used
-    if (q < 0 && !has_top) q = 0;                            // edge clamp (np.pad "edge")
-    if (q >= rows && !has_bot) q = rows - 1;
-    ld16<T>(x[r], s + (int64_t)q * M);
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (r < nr) ld16<T>(pw[r], power + (int64_t)(i0 + r) * M + m);
-  int j = 0, l = 0;
-  if (D3) {
-    j = (int)(m / L);
-    l = (int)(m - (int64_t)j * L);
+    q = q < qlo ? qlo : (q > qhi ? qhi : q);
+    ld16<T>(x[r], src + q * M + m);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     if (r >= nr) break;
     const int i = i0 + r;
-    const T *si = s + (int64_t)i * M;
+    const T *si = src + i * M + m;
     const T(&c)[V] = x[r + 1];
     T out[V];
+    const T zl = si[ozl], zr = si[ozr];
     if (D3) {
       T ym[V], yp[V];
-      if (j > 0) ld16<T>(ym, si - L); else for (int e = 0; e < V; ++e) ym[e] = c[e];
-      if (j < C - 1) ld16<T>(yp, si + L); else for (int e = 0; e < V; ++e) yp[e] = c[e];
-      const T zl = l > 0 ? si[-1] : c[0];
-      const T zr = l + V < L ? si[V] : c[V - 1];
+      ld16<T>(ym, si + oym);
+      ld16<T>(yp, si + oyp);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         const T zm = e > 0 ? c[e - 1] : zl;
@@ -224,16 +234,14 @@ __global__ void __launch_bounds__(256)
         out[e] = hotspot_cell<T, true>(x[r][e], c[e], x[r + 2][e], ym[e], yp[e], zm, zp, pw[r][e], k, loss);
       }
     } else {
-      const T yl = m > 0 ? si[-1] : c[0];
-      const T yr = m + V < M ? si[V] : c[V - 1];
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        const T a = e > 0 ? c[e - 1] : yl;
-        const T b = e < V - 1 ? c[e + 1] : yr;
+        const T a = e > 0 ? c[e - 1] : zl;
+        const T b = e < V - 1 ? c[e + 1] : zr;
         out[e] = hotspot_cell<T, false>(x[r][e], c[e], x[r + 2][e], a, b, T(0), T(0), pw[r][e], k, loss);
       }
     }
-    st16<T>(dst + (int64_t)i * M + m, out);
+    st16<T>(dst + i * M + m, out);
     if (i == 0 && halo_up) st16<T>(halo_up + m, out);
     if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
   }
@@ -414,208 +422,11 @@ __global__ void __launch_bounds__(256)
 // E half-step (workloads.py:372-412): interior update, tangential wall components written 0
 // (the reference's copy-then-zero, fused; equivalence in SURVEY.md App. B.3).
 // ================================================================================================
-template <typename T>
-__device__ __forceinline__ T curl_update(T f, T c, T p, T q, T r, T s, T d, bool unit_d) {
-  T a = rn<T>::sub(p, q);
-  T b = rn<T>::sub(r, s);
-  if (!unit_d) {
-    a = rn<T>::div(a, d);
-    b = rn<T>::div(b, d);
-  }
-  return rn<T>::add(f, rn<T>::mul(c, rn<T>::sub(a, b)));
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256)
-    k_fdtd_h(const T *__restrict__ ex, const T *__restrict__ ey, const T *__restrict__ ez,
-             T *__restrict__ hx, T *__restrict__ hy, T *__restrict__ hz, int nx, int ny, int nz,
-             T c_h, T d, int unit_d) {
-  pdl_trigger();
-  const int pw = nz + 1;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
-  pdl_wait();
-  if (p >= (int64_t)(ny + 1) * pw) return;
-  const int j = (int)(p / pw);
-  const int k = (int)(p - (int64_t)j * pw);
-  // strides
-  const int64_t ex_j = nz + 1, ex_i = (int64_t)(ny + 1) * (nz + 1);
-  const int64_t ey_j = nz + 1, ey_i = (int64_t)ny * (nz + 1);
-  const int64_t ez_j = nz, ez_i = (int64_t)(ny + 1) * nz;
-  const bool ud = unit_d != 0;
-  if (j < ny && k < nz) {  // hx[i,j,k], i <= nx
-    const int64_t h = ((int64_t)i * ny + j) * nz + k;
-    const int64_t a = i * ey_i + j * ey_j + k;
-    const int64_t b = i * ez_i + j * ez_j + k;
-    hx[h] = curl_update<T>(hx[h], c_h, ey[a + 1], ey[a], ez[b + ez_j], ez[b], d, ud);
-  }
-  if (i < nx && k < nz) {  // hy[i,j,k], j <= ny
-    const int64_t h = ((int64_t)i * (ny + 1) + j) * nz + k;
-    const int64_t a = i * ez_i + j * ez_j + k;
-    const int64_t b = i * ex_i + j * ex_j + k;
-    hy[h] = curl_update<T>(hy[h], c_h, ez[a + ez_i], ez[a], ex[b + 1], ex[b], d, ud);
-  }
-  if (i < nx && j < ny) {  // hz[i,j,k], k <= nz
-    const int64_t h = ((int64_t)i * ny + j) * (nz + 1) + k;
-    const int64_t a = i * ex_i + j * ex_j + k;
-    const int64_t b = i * ey_i + j * ey_j + k;
-    hz[h] = curl_update<T>(hz[h], c_h, ex[a + ex_j], ex[a], ey[b + ey_i], ey[b], d, ud);
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256)
-    k_fdtd_e(T *__restrict__ ex, T *__restrict__ ey, T *__restrict__ ez, const T *__restrict__ hx,
-             const T *__restrict__ hy, const T *__restrict__ hz, int nx, int ny, int nz, T c_e,
-             T d, int unit_d) {
-  pdl_trigger();
-  const int pw = nz + 1;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
-  pdl_wait();
-  if (p >= (int64_t)(ny + 1) * pw) return;
-  const int j = (int)(p / pw);
-  const int k = (int)(p - (int64_t)j * pw);
-  const int64_t hx_j = nz, hx_i = (int64_t)ny * nz;
-  const int64_t hy_j = nz, hy_i = (int64_t)(ny + 1) * nz;
-  const int64_t hz_j = nz + 1, hz_i = (int64_t)ny * (nz + 1);
-  const bool ud = unit_d != 0;
-  const T zero = T(0);
-  if (i < nx) {  // ex[i,j,k]: interior j in [1,ny-1], k in [1,nz-1]; walls j in {0,ny}, k in {0,nz}
-    const int64_t e = ((int64_t)i * (ny + 1) + j) * (nz + 1) + k;
-    if (j >= 1 && j <= ny - 1 && k >= 1 && k <= nz - 1) {
-      const int64_t a = i * hz_i + j * hz_j + k;
-      const int64_t b = i * hy_i + j * hy_j + k;
-      ex[e] = curl_update<T>(ex[e], c_e, hz[a], hz[a - hz_j], hy[b], hy[b - 1], d, ud);
-    } else {
-      ex[e] = zero;
-    }
-  }
-  if (j < ny) {  // ey[i,j,k]: interior i in [1,nx-1], k in [1,nz-1]
-    const int64_t e = ((int64_t)i * ny + j) * (nz + 1) + k;
-    if (i >= 1 && i <= nx - 1 && k >= 1 && k <= nz - 1) {
-      const int64_t a = i * hx_i + j * hx_j + k;
-      const int64_t b = i * hz_i + j * hz_j + k;
-      ey[e] = curl_update<T>(ey[e], c_e, hx[a], hx[a - 1], hz[b], hz[b - hz_i], d, ud);
-    } else {
-      ey[e] = zero;
-    }
-  }
-  if (k < nz) {  // ez[i,j,k]: interior i in [1,nx-1], j in [1,ny-1]
-    const int64_t e = ((int64_t)i * (ny + 1) + j) * nz + k;
-    if (i >= 1 && i <= nx - 1 && j >= 1 && j <= ny - 1) {
-      const int64_t a = i * hy_i + j * hy_j + k;
-      const int64_t b = i * hx_i + j * hx_j + k;
-      ez[e] = curl_update<T>(ez[e], c_e, hy[a], hy[a - hy_i], hx[b], hx[b - hx_j], d, ud);
-    } else {
-      ez[e] = zero;
-    }
-  }
-}
-
 // ================================================================================================
-// FDTD, x-marching variants. One thread per (j,k) point of the unified (ny+1) x (nz+1) plane walks
-// a chunk of x-planes: all index arithmetic is done once, every step only advances six pointers
-// by their plane strides, and the x-neighbours the update re-reads (ey/ez at i for H, hz/hy at
-// i-1 for E) are carried in registers from the previous step. Same arithmetic as k_fdtd_h/_e.
-// grid = (ceil((ny+1)(nz+1)/256), ceil(planes / planes_per_cta)).
-// ================================================================================================
-template <typename T>
-__global__ void __launch_bounds__(256)
-    k_fdtd_h_march(const T *__restrict__ ex, const T *__restrict__ ey, const T *__restrict__ ez,
-                   T *__restrict__ hx, T *__restrict__ hy, T *__restrict__ hz, int nx, int ny, int nz,
-                   int planes_per_cta, T c_h, T d, int unit_d) {
-  pdl_trigger();
-  const int pw = nz + 1;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i0 = blockIdx.y * planes_per_cta;
-  const int i1 = min(nx + 1, i0 + planes_per_cta);
-  pdl_wait();
-  if (p >= (ny + 1) * pw) return;
-  const int j = p / pw;
-  const int k = p - j * pw;
-  const bool ud = unit_d != 0;
-  const bool bx = j < ny && k < nz, by = k < nz, bz = j < ny;
-  const int64_t exs = (int64_t)(ny + 1) * (nz + 1), eys = (int64_t)ny * (nz + 1), ezs = (int64_t)(ny + 1) * nz;
-  const int64_t hxs = (int64_t)ny * nz, hys = (int64_t)(ny + 1) * nz, hzs = (int64_t)ny * (nz + 1);
-  const T *pex = ex + i0 * exs + (int64_t)j * (nz + 1) + k;
-  const T *pey = ey + i0 * eys + (int64_t)j * (nz + 1) + k;
-  const T *pez = ez + i0 * ezs + (int64_t)j * nz + k;
-  T *phx = hx + i0 * hxs + (int64_t)j * nz + k;
-  T *phy = hy + i0 * hys + (int64_t)j * nz + k;
-  T *phz = hz + i0 * hzs + (int64_t)j * (nz + 1) + k;
-  T ey_c = bz ? pey[0] : T(0);  // ey[i][j][k]
-  T ez_c = by ? pez[0] : T(0);  // ez[i][j][k]
-  for (int i = i0; i < i1; ++i) {
-    if (bx) *phx = curl_update<T>(*phx, c_h, pey[1], ey_c, pez[nz], ez_c, d, ud);
-    if (i < nx) {
-      const T ez_n = by ? pez[ezs] : T(0);  // ez[i+1][j][k]
-      const T ey_n = bz ? pey[eys] : T(0);  // ey[i+1][j][k]
-      const T exc = pex[0];
-      if (by) *phy = curl_update<T>(*phy, c_h, ez_n, ez_c, pex[1], exc, d, ud);
-      if (bz) *phz = curl_update<T>(*phz, c_h, pex[nz + 1], exc, ey_n, ey_c, d, ud);
-      ey_c = ey_n;
-      ez_c = ez_n;
-    }
-    pex += exs; pey += eys; pez += ezs;
-    phx += hxs; phy += hys; phz += hzs;
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256)
-    k_fdtd_e_march(T *__restrict__ ex, T *__restrict__ ey, T *__restrict__ ez,
-                   const T *__restrict__ hx, const T *__restrict__ hy, const T *__restrict__ hz,
-                   int nx, int ny, int nz, int planes_per_cta, T c_e, T d, int unit_d) {
-  pdl_trigger();
-  const int pw = nz + 1;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i0 = blockIdx.y * planes_per_cta;
-  const int i1 = min(nx + 1, i0 + planes_per_cta);
-  pdl_wait();
-  if (p >= (ny + 1) * pw) return;
-  const int j = p / pw;
-  const int k = p - j * pw;
-  const bool ud = unit_d != 0;
-  const int64_t exs = (int64_t)(ny + 1) * (nz + 1), eys = (int64_t)ny * (nz + 1), ezs = (int64_t)(ny + 1) * nz;
-  const int64_t hxs = (int64_t)ny * nz, hys = (int64_t)(ny + 1) * nz, hzs = (int64_t)ny * (nz + 1);
-  T *pex = ex + i0 * exs + (int64_t)j * (nz + 1) + k;
-  T *pey = ey + i0 * eys + (int64_t)j * (nz + 1) + k;
-  T *pez = ez + i0 * ezs + (int64_t)j * nz + k;
-  const T *phx = hx + i0 * hxs + (int64_t)j * nz + k;
-  const T *phy = hy + i0 * hys + (int64_t)j * nz + k;
-  const T *phz = hz + i0 * hzs + (int64_t)j * (nz + 1) + k;
-  const bool jin = j >= 1 && j <= ny - 1, kin = k >= 1 && k <= nz - 1;
-  const bool ex_upd = jin && kin;   // ex interior in (j,k)
-  const bool ey_col = j < ny, ez_col = k < nz;
-  // hz[i-1][j][k] and hy[i-1][j][k], carried down the march
-  T hz_p = (i0 >= 1 && i0 - 1 < nx && j < ny) ? phz[-hzs] : T(0);
-  T hy_p = (i0 >= 1 && i0 - 1 < nx && k < nz) ? phy[-hys] : T(0);
-  const T zero = T(0);
-  for (int i = i0; i < i1; ++i) {
-    const bool iin = i >= 1 && i <= nx - 1;
-    const T hz_c = (i < nx && j < ny) ? phz[0] : zero;
-    const T hy_c = (i < nx && k < nz) ? phy[0] : zero;
-    if (i < nx)
-      *pex = ex_upd ? curl_update<T>(*pex, c_e, hz_c, phz[-(nz + 1)], hy_c, phy[-1], d, ud) : zero;
-    if (ey_col)
-      *pey = (iin && kin) ? curl_update<T>(*pey, c_e, phx[0], phx[-1], hz_c, hz_p, d, ud) : zero;
-    if (ez_col)
-      *pez = (iin && jin) ? curl_update<T>(*pez, c_e, hy_c, hy_p, phx[0], phx[-nz], d, ud) : zero;
-    hz_p = hz_c;
-    hy_p = hy_c;
-    pex += exs; pey += eys; pez += ezs;
-    phx += hxs; phy += hys; phz += hzs;
-  }
-}
-
-// ================================================================================================
-// FDTD, lean lattice kernels (default). block = (32 along z, 8 along y), grid = (z-tiles, y-tiles,
-// nx+1): no integer division, 32-bit offsets (the launch layer checks every field has < 2^31
-// elements), and the cell size folded in at compile time (UNIT_D: /d skipped, exact for d == 1).
-// Every load of a thread is independent, so a fully occupied SM keeps ~12 loads per thread in
-// flight. Offsets: A = ex-shaped (ny+1, nz+1) rows, B = (ny, nz+1) rows (ey, hz),
-//                  Cc = (ny+1, nz) rows (ez, hy), D = (ny, nz) rows (hx).
+// FDTD, lean lattice kernels (the fallback for z rows too long for k_fdtd_lf's CTA). One thread
+// per lattice point, block = (32 along z, 8 along y), grid = (z-tiles, y-tiles, nx+1); every
+// field on the padded lattice (row pitch P, field stride FS), updated in place: H half-step then
+// E half-step, 2 launches per iteration. All 12 loads of a thread are issued before any use.
 // ================================================================================================
 // Compiler barrier that needs its operands in registers: every load feeding it is issued before
 // it, so independent loads are in flight together instead of being sunk into the branches that
@@ -641,75 +452,67 @@ __device__ __forceinline__ T curl2(T f, T c, T p, T q, T r, T s, T d) {
 
 template <typename T, bool UNIT_D>
 __global__ void __launch_bounds__(256)
-    k_fdtd_h2(const T *__restrict__ ex, const T *__restrict__ ey, const T *__restrict__ ez,
-              T *__restrict__ hx, T *__restrict__ hy, T *__restrict__ hz, int nx, int ny, int nz,
-              T c_h, T d) {
+    k_fdtd_h2(T *f, int nx, int ny, int nz, int P, int64_t FS, T c_h, T d) {
   pdl_trigger();
   const int k = blockIdx.x * 32 + threadIdx.x;
   const int j = blockIdx.y * 8 + threadIdx.y;
   const int i = blockIdx.z;
   pdl_wait();
   if (k > nz || j > ny) return;
-  const int nz1 = nz + 1, ny1 = ny + 1;
-  const int A = (i * ny1 + j) * nz1 + k;
-  const int B = (i * ny + j) * nz1 + k;
-  const int Cc = (i * ny1 + j) * nz + k;
-  const int D = (i * ny + j) * nz + k;
+  const int64_t o = ((int64_t)i * (ny + 1) + j) * P + k, rowp = P, plane = (int64_t)(ny + 1) * P;
+  const T *ex = f, *ey = f + FS, *ez = f + 2 * FS;
+  T *hx = f + 3 * FS, *hy = f + 4 * FS, *hz = f + 5 * FS;
   const bool ux = j < ny && k < nz;  // hx[i,j,k] (i <= nx always)
   const bool uy = i < nx && k < nz;  // hy[i,j,k]
   const bool uz = i < nx && j < ny;  // hz[i,j,k]
-  // issue every load before any use: ~12 independent loads in flight per thread
-  const T hx0 = ux ? hx[D] : T(0), hy0 = uy ? hy[Cc] : T(0), hz0 = uz ? hz[B] : T(0);
-  const T ey_b = (ux || uz) ? ey[B] : T(0);
-  const T ey_k = ux ? ey[B + 1] : T(0);
-  const T ey_i = uz ? ey[B + ny * nz1] : T(0);
-  const T ez_c = (ux || uy) ? ez[Cc] : T(0);
-  const T ez_j = ux ? ez[Cc + nz] : T(0);
-  const T ez_i = uy ? ez[Cc + ny1 * nz] : T(0);
-  const T ex_a = (uy || uz) ? ex[A] : T(0);
-  const T ex_k = uy ? ex[A + 1] : T(0);
-  const T ex_j = uz ? ex[A + nz1] : T(0);
+  const T hx0 = ux ? hx[o] : T(0), hy0 = uy ? hy[o] : T(0), hz0 = uz ? hz[o] : T(0);
+  const T ey_b = (ux || uz) ? ey[o] : T(0);
+  const T ey_k = ux ? ey[o + 1] : T(0);
+  const T ey_i = uz ? ey[o + plane] : T(0);
+  const T ez_c = (ux || uy) ? ez[o] : T(0);
+  const T ez_j = ux ? ez[o + rowp] : T(0);
+  const T ez_i = uy ? ez[o + plane] : T(0);
+  const T ex_a = (uy || uz) ? ex[o] : T(0);
+  const T ex_k = uy ? ex[o + 1] : T(0);
+  const T ex_j = uz ? ex[o + rowp] : T(0);
   pin(hx0, hy0, hz0, ey_b, ey_k, ey_i, ez_c, ez_j, ez_i, ex_a, ex_k, ex_j);
-  if (ux) hx[D] = curl2<T, UNIT_D>(hx0, c_h, ey_k, ey_b, ez_j, ez_c, d);   // ey(k+1)-ey, ez(j+1)-ez
-  if (uy) hy[Cc] = curl2<T, UNIT_D>(hy0, c_h, ez_i, ez_c, ex_k, ex_a, d);  // ez(i+1)-ez, ex(k+1)-ex
-  if (uz) hz[B] = curl2<T, UNIT_D>(hz0, c_h, ex_j, ex_a, ey_i, ey_b, d);   // ex(j+1)-ex, ey(i+1)-ey
+  if (ux) hx[o] = curl2<T, UNIT_D>(hx0, c_h, ey_k, ey_b, ez_j, ez_c, d);  // ey(k+1)-ey, ez(j+1)-ez
+  if (uy) hy[o] = curl2<T, UNIT_D>(hy0, c_h, ez_i, ez_c, ex_k, ex_a, d);  // ez(i+1)-ez, ex(k+1)-ex
+  if (uz) hz[o] = curl2<T, UNIT_D>(hz0, c_h, ex_j, ex_a, ey_i, ey_b, d);  // ex(j+1)-ex, ey(i+1)-ey
 }
 
 template <typename T, bool UNIT_D>
 __global__ void __launch_bounds__(256)
-    k_fdtd_e2(T *__restrict__ ex, T *__restrict__ ey, T *__restrict__ ez, const T *__restrict__ hx,
-              const T *__restrict__ hy, const T *__restrict__ hz, int nx, int ny, int nz, T c_e, T d) {
+    k_fdtd_e2(T *f, int nx, int ny, int nz, int P, int64_t FS, T c_e, T d) {
   pdl_trigger();
   const int k = blockIdx.x * 32 + threadIdx.x;
   const int j = blockIdx.y * 8 + threadIdx.y;
   const int i = blockIdx.z;
   pdl_wait();
   if (k > nz || j > ny) return;
-  const int nz1 = nz + 1, ny1 = ny + 1;
-  const int A = (i * ny1 + j) * nz1 + k;
-  const int B = (i * ny + j) * nz1 + k;
-  const int Cc = (i * ny1 + j) * nz + k;
-  const int D = (i * ny + j) * nz + k;
+  const int64_t o = ((int64_t)i * (ny + 1) + j) * P + k, rowp = P, plane = (int64_t)(ny + 1) * P;
+  T *ex = f, *ey = f + FS, *ez = f + 2 * FS;
+  const T *hx = f + 3 * FS, *hy = f + 4 * FS, *hz = f + 5 * FS;
   const bool iin = i >= 1 && i < nx, jin = j >= 1 && j < ny, kin = k >= 1 && k < nz;
   const bool wx = i < nx, wy = j < ny, wz = k < nz;  // the component exists here
   const bool ux = wx && jin && kin;                   // interior: updated (else wall: written 0)
   const bool uy = wy && iin && kin;
   const bool uz = wz && iin && jin;
-  const T ex0 = ux ? ex[A] : T(0), ey0 = uy ? ey[B] : T(0), ez0 = uz ? ez[Cc] : T(0);
-  const T hz_b = (ux || uy) ? hz[B] : T(0);
-  const T hz_j = ux ? hz[B - nz1] : T(0);
-  const T hz_i = uy ? hz[B - ny * nz1] : T(0);
-  const T hy_c = (ux || uz) ? hy[Cc] : T(0);
-  const T hy_k = ux ? hy[Cc - 1] : T(0);
-  const T hy_i = uz ? hy[Cc - ny1 * nz] : T(0);
-  const T hx_d = (uy || uz) ? hx[D] : T(0);
-  const T hx_k = uy ? hx[D - 1] : T(0);
-  const T hx_j = uz ? hx[D - nz] : T(0);
+  const T ex0 = ux ? ex[o] : T(0), ey0 = uy ? ey[o] : T(0), ez0 = uz ? ez[o] : T(0);
+  const T hz_b = (ux || uy) ? hz[o] : T(0);
+  const T hz_j = ux ? hz[o - rowp] : T(0);
+  const T hz_i = uy ? hz[o - plane] : T(0);
+  const T hy_c = (ux || uz) ? hy[o] : T(0);
+  const T hy_k = ux ? hy[o - 1] : T(0);
+  const T hy_i = uz ? hy[o - plane] : T(0);
+  const T hx_d = (uy || uz) ? hx[o] : T(0);
+  const T hx_k = uy ? hx[o - 1] : T(0);
+  const T hx_j = uz ? hx[o - rowp] : T(0);
   pin(ex0, ey0, ez0, hz_b, hz_j, hz_i, hy_c, hy_k, hy_i, hx_d, hx_k, hx_j);
   const T zero = T(0);
-  if (wx) ex[A] = ux ? curl2<T, UNIT_D>(ex0, c_e, hz_b, hz_j, hy_c, hy_k, d) : zero;  // hz(j)-hz(j-1), hy(k)-hy(k-1)
-  if (wy) ey[B] = uy ? curl2<T, UNIT_D>(ey0, c_e, hx_d, hx_k, hz_b, hz_i, d) : zero;  // hx(k)-hx(k-1), hz(i)-hz(i-1)
-  if (wz) ez[Cc] = uz ? curl2<T, UNIT_D>(ez0, c_e, hy_c, hy_i, hx_d, hx_j, d) : zero; // hy(i)-hy(i-1), hx(j)-hx(j-1)
+  if (wx) ex[o] = ux ? curl2<T, UNIT_D>(ex0, c_e, hz_b, hz_j, hy_c, hy_k, d) : zero;  // hz(j)-hz(j-1), hy(k)-hy(k-1)
+  if (wy) ey[o] = uy ? curl2<T, UNIT_D>(ey0, c_e, hx_d, hx_k, hz_b, hz_i, d) : zero;  // hx(k)-hx(k-1), hz(i)-hz(i-1)
+  if (wz) ez[o] = uz ? curl2<T, UNIT_D>(ez0, c_e, hy_c, hy_i, hx_d, hx_j, d) : zero; // hy(i)-hy(i-1), hx(j)-hx(j-1)
 }
 
 // ================================================================================================
@@ -742,11 +545,18 @@ __global__ void __launch_bounds__(256)
 // without writing, to seed the carry.
 // ================================================================================================
 constexpr int kLfMaxThreads = 384;  // (TJ+1) x groups-per-row threads, rounded up to warps
+// MODE: kLfFused (above), kLfH / kLfE = the H or the E half-step alone, in place (src == dst),
+// the two-launch leapfrog of the reference's program (workloads.py:325-413). Same staging and
+// march; H alone skips the seed plane and the E phase, E alone loads H instead of computing it and
+// needs no E_old(i+1) stage. In place is race-free: a CTA writes only its own rows, and the halo
+// rows it stages from a neighbour's tile are rows of the other field kind (not written by this
+// launch) or rows it never uses (H halo in the H launch, E halo in the E launch).
+constexpr int kLfFused = 0, kLfH = 1, kLfE = 2;
 
-template <typename T, bool UNIT_D, int TJ>
+template <typename T, bool UNIT_D, int TJ, int MODE>
 __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
-    k_fdtd_lf(const T *__restrict__ src, T *__restrict__ dst, int nx, int ny, int nz, int P,
-              int64_t FS, int tiles, int chunks, int nstages, T c_h, T c_e, T d) {
+    k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int tiles, int chunks,
+              int nstages, T c_h, T c_e, T d) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int V = 16 / sizeof(T);
   constexpr int ER = TJ + 2, HR = TJ + 1;  // E rows / H rows per stage
@@ -792,8 +602,9 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
     // tile rows [j0, j0 + h), h <= TJ: the (ny+1) rows split evenly over `tiles` tiles
     const int j0 = (int)((int64_t)(ny + 1) * tile / tiles);
     const int h = (int)((int64_t)(ny + 1) * (tile + 1) / tiles) - j0;
-    const int ib = i0 > 0 ? i0 - 1 : 0;
-    const int nload = min(i1, nx) - ib + 1;  // stages: planes ib .. min(i1, nx)
+    const int ib = (MODE != kLfH && i0 > 0) ? i0 - 1 : i0;  // seed plane for the H(i-1) carry
+    // stages: planes ib .. min(i1, nx) (E_old(i+1) of the last plane), E alone: ib .. i1-1
+    const int nload = MODE == kLfE ? i1 - ib : min(i1, nx) - ib + 1;
     const int elo = max(j0 - 1, 0), ehi = min(j0 + h, ny), hhi = min(j0 + h - 1, ny);
     const uint32_t ebytes = (uint32_t)((ehi - elo + 1) * P * sizeof(T));
     const uint32_t hbytes = (uint32_t)((hhi - elo + 1) * P * sizeof(T));
@@ -826,15 +637,23 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
       const int t = i - ib;
       const bool write = i >= i0;
       const uint32_t gs = g_base + t;
-      if (t == 0) mbar_wait(&bar[gs % nstages], (gs / nstages) & 1);
-      if (t + 1 < nload) mbar_wait(&bar[(gs + 1) % nstages], ((gs + 1) / nstages) & 1);
+      if (t == 0 || MODE == kLfE) mbar_wait(&bar[gs % nstages], (gs / nstages) & 1);
+      if (MODE != kLfE && t + 1 < nload) mbar_wait(&bar[(gs + 1) % nstages], ((gs + 1) / nstages) & 1);
       const T *Ec = ring + (size_t)(gs % nstages) * stage + r * P + k0;  // E_old(i), my row/group
       const T *En = ring + (size_t)((gs + 1) % nstages) * stage + r * P + k0;  // E_old(i+1)
       T *Hr = ring + (size_t)(gs % nstages) * stage + 3 * ER * P + r * P + k0;  // H(i), my row/group
       const bool ilt = i < nx, iin = i >= 1 && i < nx;
       T exr[V], eyr[V], ezr[V], hx[V], hy[V], hz[V];
       // ---- phase H --------------------------------------------------------------------------
-      if (row_ok) {
+      if (MODE == kLfE && row_ok) {  // H is input: this launch's H_new is the H launch's output
+        ld16<T>(exr, Ec);
+        ld16<T>(eyr, Ec + ER * P);
+        ld16<T>(ezr, Ec + 2 * ER * P);
+        ld16<T>(hx, Hr);
+        ld16<T>(hy, Hr + HR * P);
+        ld16<T>(hz, Hr + 2 * HR * P);
+      }
+      if (MODE != kLfE && row_ok && (MODE == kLfFused || r >= 1)) {
         T exd[V], ezd[V], eyn[V], ezn[V];
         ld16<T>(exr, Ec);
         ld16<T>(eyr, Ec + ER * P);
@@ -863,9 +682,11 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
           hy[e] = (ilt && klt[e]) ? b : T(0);
           hz[e] = (ilt && jlt && kle[e]) ? c : T(0);
         }
-        st16<T>(Hr, hx);
-        st16<T>(Hr + HR * P, hy);
-        st16<T>(Hr + 2 * HR * P, hz);
+        if (MODE == kLfFused) {
+          st16<T>(Hr, hx);
+          st16<T>(Hr + HR * P, hy);
+          st16<T>(Hr + 2 * HR * P, hz);
+        }
         if (write && r >= 1) {
           T *o = dst + ((int64_t)i * ny1 + jj) * P + k0;
           st16<T>(o + 3 * FS, hx);
@@ -879,7 +700,7 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
         issue(t - 1 + nstages);
       }
       // ---- phase E (owned rows) ---------------------------------------------------------------
-      if (row_ok && r >= 1) {
+      if (MODE != kLfH && row_ok && r >= 1) {
         if (write) {
           T hzu[V], hxu[V], ex[V], ey[V], ez[V];
           ld16<T>(hxu, Hr - P);               // row j-1

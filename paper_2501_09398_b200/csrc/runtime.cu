@@ -330,7 +330,8 @@ HotKernel hotspot_variant(const ib_ctx *c, int rows) {
   const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
   const int64_t M = c->plane();
   const int64_t L = d3 ? c->dims[2] : 1;
-  const bool vec_ok = (M % V == 0) && (!d3 || L % V == 0) && rows <= 65535;
+  const bool vec_ok = (M % V == 0) && (!d3 || L % V == 0) && rows <= 65535 &&
+                      (int64_t)(rows + 2) * M < (1LL << 31);  // 32-bit offsets
   const bool tma_ok = vec_ok && tma_groups<T>(c) > 0 && rows >= 2;
   const char *force = env_str("IB_HOTSPOT_KERNEL");
   if (force) {
@@ -383,17 +384,17 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     dim3 block(256);
     switch (hotspot_variant<T>(c, rows)) {
       case HotKernel::Vec: {
-        // rows per thread (R+2 row loads per R outputs): the smallest R whose grid fits in one
-        // wave of resident CTAs — a partial second wave costs a whole wave of latency on these
-        // launch-bound grids (measured: Hotspot3D 512x512x8 2048 CTAs -> 1024 CTAs, -8%).
-        // IB_HOTSPOT_VEC_ROWS overrides.
+        // rows per thread (R+2 row loads per R outputs): R = 1 (the most threads, the shortest
+        // per-thread chain) unless the grid would exceed two waves of resident CTAs. Measured
+        // in-graph with programmatic edges (us/iter): Hotspot3D 512x512x8 R=1 4.41, R=2 4.57,
+        // R=4 4.67; Hotspot2D 1024^2 R=1 2.56, R=2 3.12. IB_HOTSPOT_VEC_ROWS overrides.
         int64_t R = env_int("IB_HOTSPOT_VEC_ROWS", 0);
         const int64_t threads_per_row = plane / V;
         const int64_t xblocks = (threads_per_row + 255) / 256;
         if (R <= 0) {
-          const int64_t slots = 8LL * c->num_sms;  // 256-thread CTAs, <= 32 regs -> 8 per SM
+          const int64_t slots = 6LL * c->num_sms;  // 256-thread CTAs at <= 40 registers
           R = 1;
-          while (R < 4 && xblocks * ((rows + R - 1) / R) > slots) R *= 2;
+          while (R < 4 && xblocks * ((rows + R - 1) / R) > 2 * slots) R *= 2;
         }
         R = R >= 4 ? 4 : (R >= 2 ? 2 : 1);
         const void *fn;
@@ -437,56 +438,6 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
       }
     }
   }
-}
-
-template <typename T>
-void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
-  const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
-  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
-  const int unit = (c->scalars[0] == 1.0) ? 1 : 0;
-  T **f = (T **)c->field;
-  const int64_t pl = (int64_t)(ny + 1) * (nz + 1);
-  dim3 block(256);
-  const char *force = env_str("IB_FDTD_KERNEL");
-  int64_t maxel = 0;
-  for (int q = 0; q < 6; ++q) maxel = std::max(maxel, numel(c->fshape[q], 3));
-  const bool lean_ok = maxel + (int64_t)(ny + 1) * (nz + 1) < (1LL << 31);
-  if (lean_ok && (!force || !std::strcmp(force, "lean"))) {
-    dim3 b2(32, 8);
-    dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)(nx + 1));
-    const void *fh = unit ? (const void *)ib::k_fdtd_h2<T, true> : (const void *)ib::k_fdtd_h2<T, false>;
-    const void *fe = unit ? (const void *)ib::k_fdtd_e2<T, true> : (const void *)ib::k_fdtd_e2<T, false>;
-    out.push_back(make_launch(fh, grid, b2, 0, (const T *)f[0], (const T *)f[1], (const T *)f[2], f[3],
-                              f[4], f[5], nx, ny, nz, ch, d));
-    out.push_back(make_launch(fe, grid, b2, 0, f[0], f[1], f[2], (const T *)f[3], (const T *)f[4],
-                              (const T *)f[5], nx, ny, nz, ce, d));
-    return;
-  }
-  const bool flat = force && !std::strcmp(force, "flat");
-  if (flat || pl > (1LL << 30)) {
-    dim3 grid((unsigned)((pl + 255) / 256), (unsigned)(nx + 1));
-    out.push_back(make_launch((const void *)ib::k_fdtd_h<T>, grid, block, 0, (const T *)f[0],
-                              (const T *)f[1], (const T *)f[2], f[3], f[4], f[5], nx, ny, nz, ch, d, unit));
-    out.push_back(make_launch((const void *)ib::k_fdtd_e<T>, grid, block, 0, f[0], f[1], f[2],
-                              (const T *)f[3], (const T *)f[4], (const T *)f[5], nx, ny, nz, ce, d, unit));
-    return;
-  }
-  // x-march: as many x-chunks as fill one wave of resident CTAs (each CTA then streams its chunk)
-  const int64_t bpp = (pl + 255) / 256;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)ib::k_fdtd_h_march<T>, 256, 0);
-  const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
-  int64_t chunks = std::max<int64_t>(1, slots / bpp);
-  int64_t ppc = env_int("IB_FDTD_PPC", 0);
-  if (ppc <= 0) ppc = (nx + 1 + chunks - 1) / chunks;
-  ppc = std::max<int64_t>(1, std::min<int64_t>(ppc, nx + 1));
-  dim3 grid((unsigned)bpp, (unsigned)((nx + 1 + ppc - 1) / ppc));
-  out.push_back(make_launch((const void *)ib::k_fdtd_h_march<T>, grid, block, 0, (const T *)f[0],
-                            (const T *)f[1], (const T *)f[2], f[3], f[4], f[5], nx, ny, nz, (int)ppc, ch,
-                            d, unit));
-  out.push_back(make_launch((const void *)ib::k_fdtd_e_march<T>, grid, block, 0, f[0], f[1], f[2],
-                            (const T *)f[3], (const T *)f[4], (const T *)f[5], nx, ny, nz, (int)ppc, ce,
-                            d, unit));
 }
 
 // Fused leapfrog (k_fdtd_lf): TJ y-rows per tile, NS-stage bulk-copy ring. The largest TJ (and
@@ -537,23 +488,32 @@ inline LfConfig lf_config(const ib_ctx *c) {
   return cfg;
 }
 
-template <typename T, bool U>
-const void *lf_fn(int tj) {
+template <typename T, bool U, int M>
+const void *lf_fn_m(int tj) {
   switch (tj) {
-    case 1: return (const void *)ib::k_fdtd_lf<T, U, 1>;
-    case 2: return (const void *)ib::k_fdtd_lf<T, U, 2>;
-    case 3: return (const void *)ib::k_fdtd_lf<T, U, 3>;
-    default: return (const void *)ib::k_fdtd_lf<T, U, 4>;
+    case 1: return (const void *)ib::k_fdtd_lf<T, U, 1, M>;
+    case 2: return (const void *)ib::k_fdtd_lf<T, U, 2, M>;
+    case 3: return (const void *)ib::k_fdtd_lf<T, U, 3, M>;
+    default: return (const void *)ib::k_fdtd_lf<T, U, 4, M>;
   }
 }
-
 template <typename T>
-void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+const void *lf_fn(bool unit, int tj, int mode) {
+  if (unit) return mode == ib::kLfH ? lf_fn_m<T, true, ib::kLfH>(tj)
+                   : mode == ib::kLfE ? lf_fn_m<T, true, ib::kLfE>(tj) : lf_fn_m<T, true, ib::kLfFused>(tj);
+  return mode == ib::kLfH ? lf_fn_m<T, false, ib::kLfH>(tj)
+         : mode == ib::kLfE ? lf_fn_m<T, false, ib::kLfE>(tj) : lf_fn_m<T, false, ib::kLfFused>(tj);
+}
+
+// One k_fdtd_lf launch of `mode` from lattice buffer `from` to `to` (equal for the in-place
+// half-steps).
+template <typename T>
+Launch lf_launch(ib_ctx *c, int mode, void *from, void *to) {
   const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
   const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
   const bool unit = c->scalars[0] == 1.0;
   const LfConfig cfg = lf_config(c);
-  const void *fn = unit ? lf_fn<T, true>(cfg.tj) : lf_fn<T, false>(cfg.tj);
+  const void *fn = lf_fn<T>(unit, cfg.tj, mode);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
   const int threads = lf_threads(c, cfg.tj);
   int per_sm = 1;
@@ -576,11 +536,40 @@ void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     chunks = 0;  // even split of the tile-major unit list over `ctas` CTAs
     ctas = std::max<int64_t>(1, std::min(ctas, tiles * (nx + 1)));
   }
-  Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), 0, (const T *)c->lat[parity],
-                         (T *)c->lat[parity ^ 1], nx, ny, nz, (int)c->lat_pitch, c->lat_fs, (int)tiles,
-                         (int)chunks, cfg.ns, ch, ce, d);
+  Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), 0, (const T *)from, (T *)to, nx,
+                         ny, nz, (int)c->lat_pitch, c->lat_fs, (int)tiles, (int)chunks, cfg.ns, ch, ce, d);
   L.smem = cfg.smem;
-  out.push_back(L);
+  return L;
+}
+
+// FDTD, the reference's two half-steps (H then E, in place on the lattice): k_fdtd_lf in its H
+// and E modes, or the lean one-thread-per-point kernels when the z rows are too long for the
+// staged kernel's CTA (or IB_FDTD_KERNEL=lean).
+template <typename T>
+void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
+  const char *force = env_str("IB_FDTD_KERNEL");
+  const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0;
+  if (!lean) {
+    out.push_back(lf_launch<T>(c, ib::kLfH, c->lat[0], c->lat[0]));
+    out.push_back(lf_launch<T>(c, ib::kLfE, c->lat[0], c->lat[0]));
+    return;
+  }
+  const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
+  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
+  const bool unit = c->scalars[0] == 1.0;
+  dim3 b2(32, 8);
+  dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)(nx + 1));
+  const void *fh = unit ? (const void *)ib::k_fdtd_h2<T, true> : (const void *)ib::k_fdtd_h2<T, false>;
+  const void *fe = unit ? (const void *)ib::k_fdtd_e2<T, true> : (const void *)ib::k_fdtd_e2<T, false>;
+  T *f = (T *)c->lat[0];
+  out.push_back(make_launch(fh, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ch, d));
+  out.push_back(make_launch(fe, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ce, d));
+}
+
+// FDTD fused: one k_fdtd_lf launch per iteration, parity -> parity ^ 1.
+template <typename T>
+void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1]));
 }
 
 void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
@@ -1024,21 +1013,24 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
       IB_CUDA(cudaMemset(s.power, 0, (size_t)(s.rows() * plane * es)));
     }
     IB_CUDA(cudaSetDevice(c->slabs[0].device));
-  } else if (c->solver == IB_SOLVER_FDTD_FUSED) {
+  } else if (c->fdtd()) {
+    // both FDTD solvers: the padded lattice (kernels.cuh, k_fdtd_lf); the fused leapfrog double
+    // buffers it, the two half-steps update one copy in place
     const int64_t nx = c->dims[0], ny = c->dims[1], nz = c->dims[2];
     const int64_t v = 16 / es;
     c->lat_pitch = (nz + 1 + v - 1) / v * v;
     c->lat_fs = (nx + 1) * (ny + 1) * c->lat_pitch;
-    if (lf_config(c).tj == 0)
+    const bool fused = c->solver == IB_SOLVER_FDTD_FUSED;
+    if (fused && lf_config(c).tj == 0)
       return fail(IB_EINVAL, "fused fdtd: the z rows are too long for one CTA (threads or shared-memory ring); use the two-kernel solver");
     const size_t b = (size_t)(6 * c->lat_fs * es);
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < (fused ? 2 : 1); ++p) {
       IB_CUDA(cudaMalloc(&c->lat[p], b));
       IB_CUDA(cudaMemset(c->lat[p], 0, b));
     }
     for (int f = 0; f < 6; ++f) {
       c->field[f] = (char *)c->lat[0] + (size_t)(f * c->lat_fs * es);
-      c->field2[f] = (char *)c->lat[1] + (size_t)(f * c->lat_fs * es);
+      if (fused) c->field2[f] = (char *)c->lat[1] + (size_t)(f * c->lat_fs * es);
     }
   } else {
     for (int f = 0; f < c->nfields; ++f) {
@@ -1292,7 +1284,7 @@ static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
   if (c->hotspot()) return hotspot_copy(c, field, host, bytes, up);
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
   void *dev = c->fieldp(field, c->cur);
-  if (c->solver == IB_SOLVER_FDTD_FUSED) {  // C-order host array <-> padded lattice
+  if (c->fdtd()) {  // C-order host array <-> padded lattice
     const int64_t *sh = c->fshape[field];
     const size_t es = (size_t)c->esize;
     cudaMemcpy3DParms m = {};

@@ -2,8 +2,10 @@
 
 The runtime chooses between kernel variants by shape and size: for hotspot the
 scalar march, the 16-byte vectorised row kernel and the cp.async.bulk (TMA) plane-march pipeline;
-for FDTD the flat lattice kernels and the x-march kernels. IB_HOTSPOT_KERNEL / IB_FDTD_KERNEL /
-IB_HOTSPOT_RPC / IB_TMA_STAGES / IB_FDTD_PPC force a choice, so each variant is checked here at
+for FDTD the staged k_fdtd_lf modes (fused, H, E) at every tile height / chunking and the lean
+fallback. IB_HOTSPOT_KERNEL / IB_HOTSPOT_VEC_ROWS / IB_HOTSPOT_RPC / IB_TMA_STAGES /
+IB_FDTD_KERNEL / IB_FDTD_TJ / IB_FDTD_CHUNKS / IB_FDTD_TILES / IB_FDTD_CTAS force a choice, so
+each variant is checked here at
 shapes its automatic choice would not reach (ragged tiles, tiny chunks, slabs, binary64).
 """
 
@@ -37,7 +39,7 @@ def env():
 
 
 HOT_SHAPES = [(64, 48), (33, 1024), (7, 4100), (1, 8), (40, 12, 8), (9, 20, 256), (5, 3, 512),
-              (17, 6, 4), (2, 2, 4)]
+              (17, 6, 4), (2, 2, 4), (11, 7, 16), (3, 1, 8), (1, 1, 16), (13, 16)]
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
@@ -67,6 +69,19 @@ def test_hotspot_tma_chunking_and_ring_depth(gpu, env, rpc, stages):
         assert np.array_equal(np.asarray(got, np.float32), want), shape
 
 
+@pytest.mark.parametrize("rows", [1, 2, 4])
+def test_hotspot_vec_rows_per_thread(gpu, env, rows):
+    """The vectorised kernel with every rows-per-thread choice, ragged last row chunk included."""
+    env(IB_HOTSPOT_KERNEL="vec", IB_HOTSPOT_VEC_ROWS=rows)
+    rng = np.random.default_rng(rows)
+    for shape in ((23, 16, 8), (30, 5, 4), (9, 3, 16), (31, 64), (6, 8)):
+        for dtype, npd in (("f32", np.float32), ("f64", np.float64)):
+            state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
+            want = ocpu.hotspot(state.temperature, state.power, 0.1, 5, npd)
+            got = wl.run_batched(wl.hotspot_program(), state, 5, 1, dtype=dtype, pdl=True).temperature
+            assert np.array_equal(np.asarray(got, npd), want), (shape, dtype)
+
+
 @pytest.mark.parametrize("kernel", ["vec", "tma", "scalar"])
 @pytest.mark.parametrize("slabs", [2, 3, 5])
 def test_hotspot_variants_with_slabs(gpu, env, kernel, slabs):
@@ -83,13 +98,15 @@ FDTD_DIMS = [(8, 4, 8), (5, 6, 7), (1, 1, 1), (3, 1, 9), (16, 9, 33), (2, 40, 3)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("kernel,ppc", [("lean", 0), ("flat", 0), ("march", 0), ("march", 1), ("march", 2),
-                                        ("march", 5)])
+@pytest.mark.parametrize("kernel,tj,chunks", [("lean", 0, 0), ("staged", 0, 0), ("staged", 1, 0),
+                                              ("staged", 2, 3), ("staged", 3, 1), ("staged", 4, 2)])
 @pytest.mark.parametrize("dims", FDTD_DIMS, ids=["x".join(map(str, d)) for d in FDTD_DIMS])
-def test_fdtd_variant_bitwise(gpu, env, dims, kernel, ppc, dtype):
-    env(IB_FDTD_KERNEL=kernel, IB_FDTD_PPC=ppc)
+def test_fdtd_variant_bitwise(gpu, env, dims, kernel, tj, chunks, dtype):
+    """The two half-step launches per iteration (in place on the padded lattice): the staged
+    k_fdtd_lf H / E modes at every tile height and chunking, and the lean fallback, == oracle."""
+    env(IB_FDTD_KERNEL=kernel, IB_FDTD_TJ=tj, IB_FDTD_CHUNKS=chunks)
     base = wl.fdtd_cavity(*dims)
-    rng = np.random.default_rng(sum(dims) + ppc)
+    rng = np.random.default_rng(sum(dims) + tj + chunks)
     state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
                             base.cell_size, base.time_step)
     npd = np.float32 if dtype == "f32" else np.float64
@@ -99,11 +116,14 @@ def test_fdtd_variant_bitwise(gpu, env, dims, kernel, ppc, dtype):
     got = wl.run_batched(wl.fdtd_program(), state, 2, 2, dtype=dtype, pdl=True)
     for g, w in zip(got.state_arrays(), want):
         assert np.array_equal(np.asarray(g, npd), w)
+    got = wl.run_loop(wl.fdtd_program(), state, 4, dtype=dtype)
+    for g, w in zip(got.state_arrays(), want):
+        assert np.array_equal(np.asarray(g, npd), w)
 
 
 def test_fdtd_non_unit_cell_size(gpu, env):
     """d != 1 exercises the division path (skipped exactly when d == 1)."""
-    for kernel in ("lean", "flat", "march"):
+    for kernel in ("lean", "staged"):
         env(IB_FDTD_KERNEL=kernel)
         w = wl.te101_cavity(6, 5, 7, cell_size=0.37)
         dt = w.time_step
@@ -112,6 +132,23 @@ def test_fdtd_non_unit_cell_size(gpu, env):
         got = wl.run_loop(wl.fdtd_program(), w, 9)
         for g, ww in zip(got.state_arrays(), want):
             assert np.array_equal(g, ww)
+
+
+def test_fdtd_long_z_rows_fall_back_to_lean(gpu):
+    """z rows too long for the staged kernel's CTA: the two-launch solver takes the lean kernels,
+    the fused solver refuses with ValueError (no silent change of algorithm)."""
+    base = wl.fdtd_cavity(2, 2, 1600)
+    rng = np.random.default_rng(5)
+    state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
+                            base.cell_size, base.time_step)
+    dt = state.time_step
+    want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
+                     dt / wl.VACUUM_PERMITTIVITY, 3, np.float32)
+    got = wl.run_loop(wl.fdtd_program(), state, 3, dtype="f32")
+    for g, w in zip(got.state_arrays(), want):
+        assert np.array_equal(np.asarray(g, np.float32), w)
+    with pytest.raises(ValueError):
+        wl.run_loop(wl.fdtd_program(), state, 3, dtype="f32", fuse=True)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])

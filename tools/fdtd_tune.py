@@ -5,14 +5,13 @@ from paper_2501_09398_b200 import cli, workloads as wl
 
 n = int(os.environ.get("N", "256"))
 st = cli.build_workload("fdtd", [n])
-variants = [("two-kernel", False, {})]
-variants.append(("fused default", True, {}))
-for tj, ns, chunks in ((4, 6, 1), (4, 6, 2), (4, 6, 3), (4, 5, 2), (3, 6, 2), (3, 4, 0), (2, 5, 0)):
-    variants.append((f"fused tj={tj} ns={ns} chunks={chunks}", True,
+variants = [("two-kernel staged (default)", False, {}), ("two-kernel lean", False, {"IB_FDTD_KERNEL": "lean"}),
+            ("fused default", True, {})]
+for tj, ns, chunks in ((4, 6, 0), (4, 5, 0), (3, 4, 0), (2, 5, 0), (3, 6, 0), (4, 6, 1)):
+    variants.append((f"two-kernel tj={tj} ns={ns} chunks={chunks}", False,
                      {"IB_FDTD_TJ": tj, "IB_FDTD_STAGES": ns, "IB_FDTD_CHUNKS": chunks}))
-variants.append(("fused even-split ctas=296", True, {"IB_FDTD_CTAS": 296}))
 for name, fuse, env in variants:
-    for k in ("IB_FDTD_TJ", "IB_FDTD_STAGES", "IB_FDTD_CTAS", "IB_FDTD_CHUNKS", "IB_FDTD_TILES"):
+    for k in ("IB_FDTD_TJ", "IB_FDTD_STAGES", "IB_FDTD_CTAS", "IB_FDTD_CHUNKS", "IB_FDTD_TILES", "IB_FDTD_KERNEL"):
         os.environ.pop(k, None)
     for k, v in env.items():
         os.environ[k] = str(v)

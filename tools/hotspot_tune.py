@@ -1,0 +1,35 @@
+"""Hotspot launch-bound configs: graph-mode (PDL, K=50) and stream us/iter per kernel variant."""
+import os, sys, statistics
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2501_09398_b200 import cli, workloads as wl
+
+KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES")
+cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
+variants = [("auto", {})]
+for r in (1, 2, 4):
+    variants.append((f"vec R={r}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r}))
+if os.environ.get("ALL"):
+    for rpc in (2, 4, 8, 16):
+        variants.append((f"tma rpc={rpc}", {"IB_HOTSPOT_KERNEL": "tma", "IB_HOTSPOT_RPC": rpc}))
+    for rpc in (2, 4, 8):
+        variants.append((f"scalar rpc={rpc}", {"IB_HOTSPOT_KERNEL": "scalar", "IB_HOTSPOT_RPC": rpc}))
+for w, size, n in cfgs:
+    st = cli.build_workload(w, size)
+    for name, env in variants:
+        for k in KEYS:
+            os.environ.pop(k, None)
+        os.environ.update({k: str(v) for k, v in env.items()})
+        s = wl.DeviceSolver(st, "f32")
+        s.run_batched(50, n // 50, pdl=True)
+        g, gp, sp = [], [], []
+        for _ in range(5):
+            s.flush_l2(); s.upload(st)
+            g.append(s.run_batched(50, n // 50, pdl=False).gpu_s / n)
+            s.flush_l2(); s.upload(st)
+            gp.append(s.run_batched(50, n // 50, pdl=True).gpu_s / n)
+            s.flush_l2(); s.upload(st)
+            sp.append(s.run_stream(n).gpu_s / n)
+        m = lambda x: 1e6 * statistics.median(x)
+        print(f"{w:9s} {name:16s} graph {m(g):6.3f}  graph+pdl {m(gp):6.3f}  stream {m(sp):6.3f}  "
+              f"ratio {statistics.median(sp)/min(statistics.median(g), statistics.median(gp)):.3f}", flush=True)
+        s.close()
