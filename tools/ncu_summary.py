@@ -38,6 +38,7 @@ REPORTS = {
     "hotspot3d_512": "hotspot3d",
     "hotspot3d_large": "hotspot3d_large",
     "fdtd": "fdtd",
+    "fdtd_fused": "fdtd_fused",
     "skeleton": "skeleton",
 }
 UNIT = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "nsecond": 1e-9,
