@@ -173,9 +173,11 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // itself — so the per-row work is 5 loads, 1 store and the cell arithmetic, with 32-bit offsets
 // (the launch layer checks the slab buffer holds < 2^31 elements).
 // Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles a
-// y-row). block = (256/RB, RB): a CTA covers RB consecutive row-blocks of one plane strip, so the
-// x-neighbour rows its warps share are L1 hits and L2 sees (RB*R+2)/(RB*R) reads of T instead of
-// (R+2)/R at the same thread count. grid = (ceil(M/V/(256/RB)), ceil(rows/(R*RB))).
+// y-row). grid = (ceil(M/V/256), ceil(rows/R)).
+// Measured alternatives that were not faster in-graph (Hotspot2D 1024^2 / Hotspot3D 512^2x8):
+// 2-D CTAs sharing x rows through L1, 2-4 warp-strided groups per thread (fewer instructions per
+// cell), a whole y-row per thread: the one-wave kernel is bound by its memory round trip and the
+// L1/TEX request rate, and fewer, fatter threads expose more latency.
 // ================================================================================================
 template <typename T, bool D3, int R>
 __global__ void __launch_bounds__(256)
@@ -186,8 +188,8 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();
   const int M = C * L;
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) * V;
-  const int i0 = (blockIdx.y * blockDim.y + threadIdx.y) * R;
-  if (m >= M || i0 >= rows) return;
+  const int i0 = blockIdx.y * R;
+  if (m >= M) return;
   const int nr = min(R, rows - i0);
   // neighbour offsets relative to the group's first cell, edge-clamped once
   int oym, oyp, ozl, ozr;  // y-1 / y+1 group, z-1 / z+1 scalar (3-D); 2-D: y is the row axis

@@ -385,7 +385,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     switch (hotspot_variant<T>(c, rows)) {
       case HotKernel::Vec: {
         // rows per thread (R+2 row loads per R outputs): R = 1 (the most threads, the shortest
-        // per-thread chain) unless the grid would exceed two waves of resident CTAs. Measured
+        // per-thread chain) unless the grid would exceed four waves of resident CTAs. Measured
         // in-graph with programmatic edges (us/iter): Hotspot3D 512x512x8 R=1 4.41, R=2 4.57,
         // R=4 4.67; Hotspot2D 1024^2 R=1 2.56, R=2 3.12. IB_HOTSPOT_VEC_ROWS overrides.
         int64_t R = env_int("IB_HOTSPOT_VEC_ROWS", 0);
@@ -394,27 +394,17 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         if (R <= 0) {
           const int64_t slots = 6LL * c->num_sms;  // 256-thread CTAs at <= 40 registers
           R = 1;
-          while (R < 4 && xblocks * ((rows + R - 1) / R) > 2 * slots) R *= 2;
+          while (R < 4 && xblocks * ((rows + R - 1) / R) > 4 * slots) R *= 2;
         }
         R = R >= 4 ? 4 : (R >= 2 ? 2 : 1);
-        // row-blocks per CTA: block (256/RB, RB) so the warps of a CTA share x-neighbour rows in
-        // L1; the largest RB <= 4 that still gives each CTA row a full 16-byte group per thread.
-        int64_t RB = env_int("IB_HOTSPOT_RB", 0);
-        if (RB <= 0) {
-          RB = 4;
-          while (RB > 1 && 256 / RB > threads_per_row) RB /= 2;
-        }
-        RB = RB >= 8 ? 8 : RB >= 4 ? 4 : RB >= 2 ? 2 : 1;
-        const int64_t bx = 256 / RB;
-        const int64_t xb = (threads_per_row + bx - 1) / bx;
         const void *fn;
         if (d3) fn = R == 4 ? (const void *)ib::k_hotspot_vec<T, true, 4>
                    : R == 2 ? (const void *)ib::k_hotspot_vec<T, true, 2> : (const void *)ib::k_hotspot_vec<T, true, 1>;
         else fn = R == 4 ? (const void *)ib::k_hotspot_vec<T, false, 4>
                   : R == 2 ? (const void *)ib::k_hotspot_vec<T, false, 2> : (const void *)ib::k_hotspot_vec<T, false, 1>;
-        dim3 grid((unsigned)xb, (unsigned)((rows + R * RB - 1) / (R * RB)));
-        out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)RB), g, src, dst, (const T *)s.power,
-                                  rows, C, L, k, loss, top, bot, up, dn));
+        dim3 grid((unsigned)xblocks, (unsigned)((rows + R - 1) / R));
+        out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, k, loss,
+                                  top, bot, up, dn));
         break;
       }
       case HotKernel::Tma: {

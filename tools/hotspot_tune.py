@@ -3,13 +3,11 @@ import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl
 
-KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES", "IB_HOTSPOT_RB")
+KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES")
 cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
 variants = [("auto", {})]
-for r in (1, 2):
-    for rb in (1, 2, 4, 8):
-        variants.append((f"vec R={r} RB={rb}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
-                                               "IB_HOTSPOT_RB": rb}))
+for r in (1, 2, 4):
+    variants.append((f"vec R={r}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r}))
 if os.environ.get("ALL"):
     for rpc in (2, 4, 8, 16):
         variants.append((f"tma rpc={rpc}", {"IB_HOTSPOT_KERNEL": "tma", "IB_HOTSPOT_RPC": rpc}))
