@@ -163,7 +163,8 @@ uint64_t ib_fnv1a64_f64(const void *values, size_t n, int dtype, uint64_t h);
  * every iteration's stencil kernel the runtime exchanges boundary planes with rank-1 / rank+1 by
  * NCCL send/recv on the launch stream (libnccl.so.2 is dlopen'ed; graphs are stream-captured, so
  * the exchange is part of the iteration-batch graph). All ranks call ib_create_dist collectively
- * with the same 128-byte id from ib_nccl_unique_id on rank 0.
+ * with the same 128-byte id from ib_nccl_unique_id on rank 0 (NCCL exchange), or with id128 =
+ * NULL and then ib_ipc_attach (peer exchange, below).
  * For these contexts ib_upload takes the slab WITH its halo rows, i.e. global rows
  * [lo - has_top, hi + has_bot) for the temperature and [lo, hi) for the power; ib_download
  * returns the owned rows [lo, hi). ib_slab_info reports lo, hi, has_top, has_bot. */
@@ -172,6 +173,21 @@ int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int
                    const double *scalars, int nscalars, int device, int rank, int nranks,
                    const void *id128);
 int ib_slab_info(const ib_ctx *ctx, int64_t *lo, int64_t *hi, int *has_top, int *has_bot);
+
+/* ---- peer halo exchange across processes (the NVLink-native alternative to NCCL) --------------
+ * Create the context with ib_create_dist(..., id128 = NULL) (no NCCL communicator), export this
+ * rank's buffers with ib_ipc_export (IB_IPC_BYTES of CUDA IPC handles: both temperature buffers
+ * and a small counter block), hand them to the neighbour ranks (any host transport; the Python
+ * layer uses torch.distributed), and ib_ipc_attach the handles of rank-1 (up) and rank+1 (down)
+ * (NULL where there is none). From then on the stencil kernel stores its first / last owned
+ * output plane straight into the neighbours' halo planes (NVLink peer stores); ordering across
+ * processes is a pair of one-thread kernels per iteration (wait for the neighbours' completed-
+ * iteration counters, publish this rank's), all inside the iteration-batch graph. A lost
+ * neighbour traps after IB_DIST_TIMEOUT_MS (default 20000) instead of hanging the device.
+ * Replaces the NCCL group of ib_create_dist(id128 != NULL). SURVEY.md §8e, v2. */
+#define IB_IPC_BYTES 192
+int ib_ipc_export(const ib_ctx *ctx, void *out, size_t bytes);
+int ib_ipc_attach(ib_ctx *ctx, const void *up_handles, const void *down_handles);
 
 /* ---- real traces (the reference's EventTrace schema, simulate.py:28-36, fileio.py:48) ---------
  * ib_trace_enable(ctx, capacity > 0) clears and arms tracing; 0 disarms. While armed (single-slab

@@ -43,6 +43,8 @@ class IbTimes(ctypes.Structure):
 _lib = None
 _lock = threading.Lock()
 
+IPC_BYTES = 192  # IB_IPC_BYTES
+
 # (name, restype, argtypes) — must match include/iterbatch_b200.h
 _P, _I, _I64, _SZ, _U64, _D = (
     ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_double,
@@ -81,6 +83,8 @@ PROTOTYPES = [
                             _I, _I, _I, _P]),
     ("ib_slab_info", _I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I),
                           ctypes.POINTER(_I)]),
+    ("ib_ipc_export", _I, [_P, _P, _SZ]),
+    ("ib_ipc_attach", _I, [_P, _P, _P]),
     ("ib_trace_enable", _I, [_P, _I64]),
     ("ib_trace_kernels", _I64, [_P, ctypes.POINTER(_I64), _I64]),
     ("ib_trace_host_events", _I64, [_P, ctypes.POINTER(_I64), _I64]),
@@ -90,6 +94,23 @@ PROTOTYPES = [
 
 class LibraryMissingError(ImportError):
     pass
+
+
+def _point_at_torch_nccl() -> None:
+    """Let the runtime dlopen the NCCL wheel torch links against (not an older system copy)."""
+    if os.environ.get("IB_NCCL_LIB"):
+        return
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["IB_NCCL_LIB"] = cand
+            return
 
 
 def lib():
@@ -104,6 +125,7 @@ def lib():
                     f"{LIB_PATH} is missing; build it with `python -m paper_2501_09398_b200.build` "
                     "(this package has no CPU fallback)"
                 )
+            _point_at_torch_nccl()
             L = ctypes.CDLL(LIB_PATH)
             for name, res, args in PROTOTYPES:
                 fn = getattr(L, name)

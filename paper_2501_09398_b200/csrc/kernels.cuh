@@ -737,6 +737,48 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
   }
 }
 
+// ---- cross-process halo ordering (peer exchange, runtime.cu: ib_ipc_attach) -------------------------
+// sync[0] = iterations this rank has completed, sync[1] / sync[2] = the up / down neighbour's,
+// written by the neighbour itself through its IPC mapping. Before iteration t's stencil kernel a
+// rank waits until both neighbours have completed t iterations: their halo planes for t are in
+// this rank's buffers (RAW) and they are done reading the planes this kernel will overwrite in
+// their buffers (WAR). After the stencil kernel, k_dist_signal publishes t+1.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spins (bounded: traps after timeout_ms so a lost neighbour fails the launch instead of hanging
+// the device) until the neighbours' completed-iteration counts reach this rank's.
+__global__ void k_dist_wait(const unsigned long long *sync, int has_top, int has_bot, long long timeout_ms) {
+  pdl_wait();
+  const unsigned long long t = ld_acquire_sys(&sync[0]);
+  const unsigned long long t0 = global_ns(), limit = (unsigned long long)timeout_ms * 1000000ull;
+  while ((has_top && ld_acquire_sys(&sync[1]) < t) || (has_bot && ld_acquire_sys(&sync[2]) < t)) {
+    __nanosleep(200);
+    if (global_ns() - t0 > limit) __trap();
+  }
+}
+
+// Publishes one more completed iteration to this rank's counter and to the neighbours' copies.
+__global__ void k_dist_signal(unsigned long long *sync, unsigned long long *up_sync, unsigned long long *dn_sync) {
+  pdl_wait();
+  __threadfence_system();  // the preceding stencil kernel's peer stores are ordered before the flag
+  const unsigned long long d = sync[0] + 1;
+  sync[0] = d;
+  if (up_sync) st_release_sys(&up_sync[2], d);  // I am the up neighbour's "down"
+  if (dn_sync) st_release_sys(&dn_sync[1], d);  // I am the down neighbour's "up"
+}
+
 // ---- utilities ---------------------------------------------------------------------------------
 // Streams a buffer larger than L2 (benchmark hygiene between timed steps).
 __global__ void k_flush(uint4 *__restrict__ buf, int64_t n16, uint32_t salt) {

@@ -144,7 +144,13 @@ struct Nccl {
 Nccl &nccl() {
   static Nccl n = [] {
     Nccl r;
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // The copy the process already holds (torch's), else IB_NCCL_LIB (the Python layer points it
+    // at the wheel torch links against, so a later `import torch` finds a compatible NCCL), else
+    // the loader's default. RTLD_LOCAL: never interpose NCCL symbols on other libraries.
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    const char *path = std::getenv("IB_NCCL_LIB");
+    if (!h && path && *path) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
       r.err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
       return r;
@@ -254,8 +260,16 @@ struct ib_ctx {
   size_t flush_bytes = 0;
   // multi-process slab (ib_create_dist)
   int rank = 0, nranks = 1;
-  void *comm = nullptr;  // ncclComm_t
-  bool dist() const { return comm != nullptr; }
+  void *comm = nullptr;  // ncclComm_t (NCCL exchange)
+  // peer exchange (ib_ipc_attach): the stencil kernel stores its boundary planes straight into the
+  // neighbour ranks' halo planes through CUDA IPC mappings; cross-process ordering by device-side
+  // iteration counters (k_dist_wait / k_dist_signal, one pair per iteration inside the graph)
+  unsigned long long *sync = nullptr;        // [0] my completed iterations, [1] up's, [2] down's
+  void *peer_buf_up[2] = {nullptr, nullptr}, *peer_buf_dn[2] = {nullptr, nullptr};
+  unsigned long long *peer_sync_up = nullptr, *peer_sync_dn = nullptr;
+  int peer_rows_up = 0;  // the up neighbour's owned rows (locates its bottom halo plane)
+  bool peer = false;
+  bool dist() const { return nranks > 1; }
   // tracing (CUPTI activity records; host events on the CUPTI timebase)
   bool tracing = false;
   int64_t trace_cap = 0;
@@ -379,6 +393,10 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     if (P > 1 && g + 1 < P) {  // my last owned row -> lower neighbour's top halo
       Slab &n = c->slabs[g + 1];
       dn = (T *)n.buf[parity ^ 1];
+    }
+    if (c->dist() && c->peer) {  // the neighbour ranks' halo planes, through IPC mappings
+      if (s.has_top) up = (T *)c->peer_buf_up[parity ^ 1] + (int64_t)(c->peer_rows_up + 1) * plane;
+      if (s.has_bot) dn = (T *)c->peer_buf_dn[parity ^ 1];
     }
     const int top = (int)s.has_top, bot = (int)s.has_bot;
     dim3 block(256);
@@ -657,6 +675,18 @@ int nccl_exchange(ib_ctx *c, int parity, cudaStream_t st) {
   return IB_OK;
 }
 
+int launch_dist_wait(ib_ctx *c, cudaStream_t st) {
+  const int top = c->slabs[0].has_top, bot = c->slabs[0].has_bot;
+  Launch L = make_launch((const void *)ib::k_dist_wait, dim3(1), dim3(1), 0, (const unsigned long long *)c->sync,
+                         top, bot, (long long)env_int("IB_DIST_TIMEOUT_MS", 20000));
+  return launch_one(L, st, false);
+}
+int launch_dist_signal(ib_ctx *c, cudaStream_t st) {
+  Launch L = make_launch((const void *)ib::k_dist_signal, dim3(1), dim3(1), 0, c->sync, c->peer_sync_up,
+                         c->peer_sync_dn);
+  return launch_one(L, st, false);
+}
+
 // Enqueue `iters` iterations starting at `parity` onto the slab streams (also used under stream
 // capture). Multi-slab: kernel(g,t) waits for kernel(g+-1,t-1) — RAW on the halo it reads and
 // WAR on the halo it writes — through double-buffered events.
@@ -682,7 +712,9 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
         }
       }
       // PDL only chains kernels on the same stream; the very first launch has no predecessor.
-      const bool use_pdl = pdl && P == 1 && (t > 0 || q > 0);
+      // Peer-exchange contexts never use it: the wait / signal kernels must not overlap the stencil.
+      const bool use_pdl = pdl && P == 1 && (t > 0 || q > 0) && !c->peer;
+      if (c->peer && q == 0) IB_TRY(launch_dist_wait(c, st));
       c->ev(single_stream ? IB_EV_NODE_ADDED : IB_EV_BASELINE_KERNEL_LAUNCHED, single_stream ? -1 : t,
             single_stream ? nk : (int64_t)q);
       IB_TRY(launch_one(L, st, use_pdl));
@@ -691,7 +723,11 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
     }
     if (c->dist()) {  // boundary planes of this iteration's output <-> neighbouring ranks
       cudaStream_t st = single_stream ? single_stream : c->slabs[0].stream;
-      IB_TRY(nccl_exchange(c, par ^ 1, st));
+      if (c->peer) {
+        IB_TRY(launch_dist_signal(c, st));  // the halo planes went out with the kernel's stores
+      } else {
+        IB_TRY(nccl_exchange(c, par ^ 1, st));
+      }
     }
     if (c->ping_pong()) par ^= 1;
   }
@@ -941,6 +977,13 @@ void ib_destroy(ib_ctx *c) {
       if (c->field2[f]) cudaFree(c->field2[f]);
     }
   }
+  for (int p = 0; p < 2; ++p) {
+    if (c->peer_buf_up[p]) cudaIpcCloseMemHandle(c->peer_buf_up[p]);
+    if (c->peer_buf_dn[p]) cudaIpcCloseMemHandle(c->peer_buf_dn[p]);
+  }
+  if (c->peer_sync_up) cudaIpcCloseMemHandle(c->peer_sync_up);
+  if (c->peer_sync_dn) cudaIpcCloseMemHandle(c->peer_sync_dn);
+  if (c->sync) cudaFree(c->sync);
   if (c->d_counter) cudaFree(c->d_counter);
   if (c->tracing) {
     Cupti &cp = cupti();
@@ -999,6 +1042,10 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   IB_CUDA(cudaEventCreate(&c->t1));
   IB_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
   IB_CUDA(cudaMalloc(&c->d_counter, sizeof(int)));
+  if (dist) {
+    IB_CUDA(cudaMalloc(&c->sync, 256));
+    IB_CUDA(cudaMemset(c->sync, 0, 256));
+  }
   const int es = c->esize;
   if (hot) {
     const int64_t plane = c->plane();
@@ -1117,7 +1164,7 @@ static int create_common(ib_ctx **out, int solver, int dtype, const int64_t *dim
     }
   }
   int rc = create_impl(c, devs.data(), (int)devs.size());
-  if (rc == IB_OK && nranks > 1) {
+  if (rc == IB_OK && nranks > 1 && id128) {
     Nccl &n = nccl();
     if (!n.ok) {
       rc = fail(IB_ECUDA, n.err);
@@ -1165,9 +1212,49 @@ int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int
   if (solver != IB_SOLVER_HOTSPOT2D && solver != IB_SOLVER_HOTSPOT3D)
     return fail(IB_EINVAL, "distributed contexts are defined for hotspot grids");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(IB_EINVAL, "bad rank / nranks");
-  if (nranks > 1 && !id128) return fail(IB_EINVAL, "nranks > 1 needs the NCCL unique id");
+
   return create_common(out, solver, dtype, dims, ndims, scalars, nscalars, &device, 1, rank, nranks,
                        id128);
+}
+
+int ib_ipc_export(const ib_ctx *c, void *out, size_t bytes) {
+  IB_TRY(check_ctx(c));
+  if (!c->dist()) return fail(IB_EINVAL, "IPC export is for distributed (ib_create_dist) contexts");
+  if (!out || bytes < IB_IPC_BYTES) return fail(IB_EINVAL, "IPC export needs IB_IPC_BYTES bytes");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  cudaIpcMemHandle_t h[3];
+  for (int p = 0; p < 2; ++p) IB_CUDA(cudaIpcGetMemHandle(&h[p], c->slabs[0].buf[p]));
+  IB_CUDA(cudaIpcGetMemHandle(&h[2], c->sync));
+  std::memcpy(out, h, sizeof(h));
+  return IB_OK;
+}
+
+int ib_ipc_attach(ib_ctx *c, const void *up, const void *dn) {
+  IB_TRY(check_ctx(c));
+  if (!c->dist()) return fail(IB_EINVAL, "IPC attach is for distributed (ib_create_dist) contexts");
+  const Slab &s = c->slabs[0];
+  if ((s.has_top && !up) || (s.has_bot && !dn))
+    return fail(IB_EINVAL, "IPC attach needs the handles of every neighbour rank");
+  if (c->peer) return fail(IB_ESTATE, "IPC peers already attached");
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(s.device));
+  auto open = [&](const void *blob, void **bufs, unsigned long long **sync) -> int {
+    cudaIpcMemHandle_t h[3];
+    std::memcpy(h, blob, sizeof(h));
+    for (int p = 0; p < 2; ++p)
+      IB_CUDA(cudaIpcOpenMemHandle(&bufs[p], h[p], cudaIpcMemLazyEnablePeerAccess));
+    void *sp = nullptr;
+    IB_CUDA(cudaIpcOpenMemHandle(&sp, h[2], cudaIpcMemLazyEnablePeerAccess));
+    *sync = (unsigned long long *)sp;
+    return IB_OK;
+  };
+  if (s.has_top) IB_TRY(open(up, c->peer_buf_up, &c->peer_sync_up));
+  if (s.has_bot) IB_TRY(open(dn, c->peer_buf_dn, &c->peer_sync_dn));
+  const int64_t rows = c->dims[0];
+  c->peer_rows_up = (int)(rows * c->rank / c->nranks - rows * (c->rank - 1) / c->nranks);
+  c->peer = true;
+  return IB_OK;
 }
 
 int ib_slab_info(const ib_ctx *c, int64_t *lo, int64_t *hi, int *has_top, int *has_bot) {
@@ -1335,6 +1422,8 @@ static int sync_all(ib_ctx *c) {
 
 int ib_run_stream(ib_ctx *c, int64_t iterations, int flags, ib_times *tm) {
   IB_TRY(check_ctx(c));
+  if (c->dist() && !c->comm && !c->peer)
+    return fail(IB_ESTATE, "distributed context without an exchange: call ib_ipc_attach first");
   if (iterations < 0) return fail(IB_EINVAL, "total_iterations must be >= 0");
   DeviceGuard guard;
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
@@ -1345,6 +1434,7 @@ int ib_run_stream(ib_ctx *c, int64_t iterations, int flags, ib_times *tm) {
   IB_CUDA(cudaEventRecord(c->t0, c->stream()));
   IB_TRY(join_into(c, c->stream(), true));
   IB_TRY(enqueue_iterations(c, iterations, c->cur, pdl, nullptr, &t.kernels, &t.launches));
+  if (c->peer && iterations > 0) IB_TRY(launch_dist_wait(c, c->stream()));
   IB_TRY(join_into(c, c->stream(), false));
   IB_CUDA(cudaEventRecord(c->t1, c->stream()));
   IB_CUDA(cudaEventSynchronize(c->t1));
@@ -1407,6 +1497,8 @@ int64_t ib_graph_batch_size(const ib_ctx *c) { return c ? c->K : -1; }
 
 int ib_graph_build(ib_ctx *c, int64_t batch_size, int build_mode, int flags, ib_times *tm) {
   IB_TRY(check_ctx(c));
+  if (c->dist() && !c->comm && !c->peer)
+    return fail(IB_ESTATE, "distributed context without an exchange: call ib_ipc_attach first");
   if (batch_size < 1) return fail(IB_EINVAL, "batch_size must be >= 1");
   if (build_mode != IB_BUILD_MANUAL && build_mode != IB_BUILD_CAPTURE)
     return fail(IB_EINVAL, "unknown build mode");
@@ -1476,6 +1568,9 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
       t.launches = num_batches;
     }
   }
+  // peer exchange: the run ends when the neighbours are done too (their last halo stores into
+  // this rank's planes have landed), so a following upload / download cannot race them
+  if (c->peer && num_batches > 0) IB_TRY(launch_dist_wait(c, c->stream()));
   IB_CUDA(cudaEventRecord(c->t1, c->stream()));
   IB_CUDA(cudaEventSynchronize(c->t1));
   auto b = clk::now();

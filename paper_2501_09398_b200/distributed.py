@@ -89,11 +89,17 @@ class DistributedSolver(DeviceSolver):
     """This rank's slab of a global hotspot grid, resident on one GPU.
 
     ``state`` is the GLOBAL HotspotWorkload (each rank only uploads its window). Graph builds
-    are stream-captured (the NCCL group is part of every iteration).
+    are stream-captured (the exchange is part of every iteration). Two exchanges:
+
+    * ``exchange="nccl"`` (``uid`` = rank 0's NCCL id): one NCCL send/recv group per iteration;
+    * ``exchange="peer"`` (``allgather`` = a callable gathering one bytes object per rank, e.g.
+      over torch.distributed): the stencil kernel stores its boundary planes straight into the
+      neighbours' halo planes through CUDA IPC mappings (NVLink peer stores), ordered across
+      processes by device-side iteration counters (include/iterbatch_b200.h, ib_ipc_attach).
     """
 
-    def __init__(self, state, dtype, rank: int, world: int, device: int, uid: bytes | None,
-                 upload: bool = True):
+    def __init__(self, state, dtype, rank: int, world: int, device: int, uid: bytes | None = None,
+                 upload: bool = True, exchange: str = "nccl", allgather=None):
         kind = _kind_of_state(state)
         if kind not in ("hotspot2d", "hotspot3d"):
             raise ValueError("distributed execution is defined for hotspot grids")
@@ -110,15 +116,22 @@ class DistributedSolver(DeviceSolver):
         ctx = ctypes.c_void_p()
         dims = (ctypes.c_int64 * len(self.dims))(*self.dims)
         sc = (ctypes.c_double * len(self.scalars))(*self.scalars)
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"exchange must be 'nccl' or 'peer', got {exchange!r}")
+        self.exchange = exchange
         idp = None
-        if world > 1:
+        if world > 1 and exchange == "nccl":
             if uid is None or len(uid) != 128:
                 raise ValueError("world > 1 needs the 128-byte NCCL unique id from rank 0")
             self._uid = ctypes.create_string_buffer(uid, 128)
             idp = ctypes.cast(self._uid, ctypes.c_void_p)
+        if world > 1 and exchange == "peer" and allgather is None:
+            raise ValueError("exchange='peer' needs an allgather callable for the IPC handles")
         _lib.check(L.ib_create_dist(ctypes.byref(ctx), _lib.SOLVER[kind], _lib.DTYPE[self.dtype], dims,
                                     len(self.dims), sc, len(self.scalars), device, rank, world, idp))
         self._ctx = ctx
+        if world > 1 and exchange == "peer":
+            self._attach_peers(allgather)
         self.nfields = 2
         plane = tuple(self.dims[1:])
         self.shapes = [(self.hi - self.lo,) + plane, (self.hi - self.lo,) + plane]
@@ -126,9 +139,31 @@ class DistributedSolver(DeviceSolver):
         if upload:
             self.upload(state)
 
+    def _attach_peers(self, allgather) -> None:
+        """Swap IPC handles with every rank and map the two neighbours' buffers."""
+        L = _lib.lib()
+        mine = ctypes.create_string_buffer(_lib.IPC_BYTES)
+        _lib.check(L.ib_ipc_export(self.ctx, ctypes.cast(mine, ctypes.c_void_p), _lib.IPC_BYTES))
+        handles = list(allgather(mine.raw))
+        if len(handles) != self.world:
+            raise RuntimeError(f"allgather returned {len(handles)} handle sets for world {self.world}")
+        keep = []
+
+        def ptr(blob):
+            if blob is None:
+                return None
+            b = ctypes.create_string_buffer(bytes(blob), _lib.IPC_BYTES)
+            keep.append(b)
+            return ctypes.cast(b, ctypes.c_void_p)
+
+        up = handles[self.rank - 1] if self.rank > 0 else None
+        dn = handles[self.rank + 1] if self.rank + 1 < self.world else None
+        _lib.check(L.ib_ipc_attach(self.ctx, ptr(up), ptr(dn)))
+
     @classmethod
     def from_seed(cls, shape, k: float, dtype, rank: int, world: int, device: int,
-                  uid: bytes | None, seed: int = 20240817) -> "DistributedSolver":
+                  uid: bytes | None, seed: int = 20240817, exchange: str = "nccl",
+                  allgather=None) -> "DistributedSolver":
         """Build this rank's slab of the reference generator's grid (cli.py:183-192) directly."""
 
         class _Shape:  # the global state's metadata only; the arrays come from seeded_window
@@ -137,7 +172,8 @@ class DistributedSolver(DeviceSolver):
                 self.power = self.temperature
                 self.diffusion_coefficient = float(k)
 
-        solver = cls(_Shape(shape, k), dtype, rank, world, device, uid, upload=False)
+        solver = cls(_Shape(shape, k), dtype, rank, world, device, uid, upload=False,
+                     exchange=exchange, allgather=allgather)
         t, p = seeded_window(shape, rank, world, seed)
         solver.upload([t, p])
         return solver

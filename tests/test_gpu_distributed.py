@@ -85,3 +85,75 @@ def test_multi_rank_nccl_halo_equals_single_gpu(gpu, shape):
     st = _state(shape)
     want = wl.run_loop(wl.hotspot_program(), st, 13, dtype="f32").temperature
     assert np.array_equal(got.astype(np.float64), want)
+
+
+def _rank_main_peer(rank, world, port, shape, kernel, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), IB_HOTSPOT_KERNEL=kernel,
+                      IB_DIST_TIMEOUT_MS="60000")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def allgather(blob):
+            out = [None] * world
+            dist.all_gather_object(out, blob)
+            return out
+
+        st = _state(shape)
+        device = rank % _lib.device_count()  # one GPU: every rank shares device 0 (IPC still works)
+        d = DistributedSolver(st, "f32", rank=rank, world=world, device=device, exchange="peer",
+                              allgather=allgather)
+        d.run_batched(5, 2)          # graph: wait / stencil with peer halo stores / signal
+        d.run_stream(3)              # stream mode, same protocol
+        first = d.local_temperature()
+        d.upload(st)                 # a second run from the initial state (counters keep going)
+        d.run_batched(4, 3, pdl=True)
+        d.run_stream(1)
+        parts = [None] * world
+        dist.all_gather_object(parts, (d.lo, d.hi, first, d.local_temperature()))
+        d.close()
+        if rank == 0:
+            a = np.empty(shape, np.float32)
+            b = np.empty(shape, np.float32)
+            for lo, hi, x, y in parts:
+                a[lo:hi] = x
+                b[lo:hi] = y
+            q.put((a, b))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kernel", ["vec", "tma", "scalar"])
+@pytest.mark.parametrize("world,shape", [(2, (64, 24, 8)), (3, (33, 40)), (2, (12, 16, 256))])
+def test_multi_rank_peer_halo_equals_single_gpu(gpu, kernel, world, shape):
+    """One process per rank, halo planes stored straight into the neighbours' buffers (CUDA IPC)
+    and ordered by device counters: == the single-domain result, bit for bit. On a one-GPU box
+    the ranks share the device (IPC between processes on one device is legal), which checks the
+    protocol, not the NVLink speed."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main_peer, args=(r, world, port, shape, kernel, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        a, b = q.get(timeout=240)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
+    st = _state(shape)
+    os.environ["IB_HOTSPOT_KERNEL"] = kernel
+    try:
+        want_a = wl.run_loop(wl.hotspot_program(), st, 13, dtype="f32").temperature
+        want_b = wl.run_loop(wl.hotspot_program(), st, 13, dtype="f32").temperature
+    finally:
+        os.environ.pop("IB_HOTSPOT_KERNEL", None)
+        wl.release_cached_contexts()
+    assert np.array_equal(a.astype(np.float64), want_a)
+    assert np.array_equal(b.astype(np.float64), want_b)
