@@ -102,6 +102,8 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--dtype", choices=["f64", "f32"], default="f64")
         p.add_argument("--build", choices=["manual", "capture"], default="manual")
         p.add_argument("--pdl", action="store_true", help="programmatic dependent launch edges")
+        p.add_argument("--fuse", action="store_true",
+                       help="fdtd: one fused kernel per iteration (H then E, double-buffered lattice)")
         p.add_argument("--devices", type=_comma_sizes, default=None,
                        help="device id per axis-0 slab (hotspot only), e.g. 0,0 or 0,1,2,3")
 
@@ -141,7 +143,7 @@ def _cmd_run_workload(args) -> int:
     program = programs()[args.workload]()
     plan = BatchPlan.from_batch_size(args.iterations, args.batch_size)
     order = wl.ExecutionOrder(args.mode)
-    kw = dict(dtype=args.dtype, devices=args.devices)
+    kw = dict(dtype=args.dtype, devices=args.devices, fuse=args.fuse)
     if args.checksum:
         if order is wl.ExecutionOrder.LOOP:
             final = wl.run_loop(program, state, plan.total_kernel_executions, pdl=args.pdl, **kw)
@@ -167,7 +169,7 @@ def _cmd_sweep(args) -> int:
     else:
         sizes = _comma_sizes(args.batch_sizes)
     os.makedirs(args.out, exist_ok=True)
-    kw = dict(dtype=args.dtype, devices=args.devices, build=args.build, pdl=args.pdl)
+    kw = dict(dtype=args.dtype, devices=args.devices, build=args.build, pdl=args.pdl, fuse=args.fuse)
     creation, execution, stream, summary = [], [], [], []
     for k in sizes:
         plan = BatchPlan.from_batch_size(total, k)
@@ -200,7 +202,8 @@ def _cmd_sweep(args) -> int:
     write_measurements_csv(MeasurementSeries(tuple(stream), label), os.path.join(args.out, "stream.csv"))
     with open(os.path.join(args.out, "summary.json"), "w") as fh:
         json.dump({"workload": args.workload, "size": args.size, "iterations": total,
-                   "dtype": args.dtype, "build": args.build, "pdl": args.pdl, "rows": summary}, fh, indent=1)
+                   "dtype": args.dtype, "build": args.build, "pdl": args.pdl, "fuse": args.fuse,
+                   "rows": summary}, fh, indent=1)
     return 0
 
 
@@ -211,7 +214,7 @@ def _cmd_trace(args) -> int:
     state = build_workload(args.workload, args.size)
     plan = BatchPlan.from_batch_size(args.iterations, args.batch_size)
     os.makedirs(args.out, exist_ok=True)
-    with wl.DeviceSolver(state, args.dtype, devices=args.devices) as s:
+    with wl.DeviceSolver(state, args.dtype, devices=args.devices, fuse=args.fuse) as s:
         s.run_batched(plan.batch_size, plan.num_batches, pdl=args.pdl)  # warm-up
         s.upload(state)
         g = tr.capture_graph(s, plan.batch_size, plan.num_batches, pdl=args.pdl)

@@ -58,9 +58,14 @@ def _arm(solver, capacity: int) -> None:
 
 
 def _arm_warm(solver, capacity: int) -> None:
-    """Arm, absorb CUPTI's one-off first-launch setup with a throwaway kernel, re-arm (clears)."""
+    """Arm, absorb CUPTI's one-off setup costs (first traced kernel launch, first traced graph
+    launch: milliseconds each) with a throwaway stream launch and a throwaway 2-iteration graph
+    (even, so the state parity is unchanged), then re-arm (clears the records)."""
     _arm(solver, capacity)
-    solver.run_stream(1)
+    solver.run_stream(2)
+    solver.build_graph(2)
+    solver.run_graph(1)
+    solver.destroy_graph()
     _arm(solver, capacity)
 
 

@@ -676,7 +676,7 @@ def run_batched(program, state, batch_size: int, num_batches: int, workers=None,
 
 
 def run_peeled(program, state, total_iterations: int, batch_size: int, workers=None, *,
-               dtype="f64", devices=None, build: str = "manual", pdl: bool = False):
+               dtype="f64", devices=None, build: str = "manual", pdl: bool = False, fuse: bool = False):
     """Any total_iterations with any batch_size: floor(N/K) graph replays plus a remainder graph.
 
     Loop peeling, the paper's remedy for the divisibility restriction that the
@@ -691,7 +691,7 @@ def run_peeled(program, state, total_iterations: int, batch_size: int, workers=N
     _check_program(program, state)
     if total == 0:
         return state
-    s = _solver_for(state, dtype, devices)
+    s = _solver_for(state, dtype, devices, fuse)
     s.run_peeled(total, size, build=build, pdl=pdl)
     return s.download(state, fields=_written_fields(state))
 
@@ -712,7 +712,7 @@ def _order_value(order) -> str:
 
 def time_workload(program, state, plan, order, repeats: int = 10, workers: int | None = None,
                   label: str = "", *, dtype="f64", devices=None, build: str = "manual",
-                  pdl: bool = False) -> MeasurementSeries:
+                  pdl: bool = False, fuse: bool = False) -> MeasurementSeries:
     """Wall-clock the full plan `repeats` times from a fresh state (workloads.py:479-505).
 
     The upload of the fresh state happens outside the timed region (the reference's state.copy()
@@ -723,14 +723,14 @@ def time_workload(program, state, plan, order, repeats: int = 10, workers: int |
         raise ValueError("repeats must be >= 1")
     _check_program(program, state)
     phases = time_workload_phases(program, state, plan, order, repeats, dtype=dtype,
-                                  devices=devices, build=build, pdl=pdl)
+                                  devices=devices, build=build, pdl=pdl, fuse=fuse)
     samples = phases["total"]
     return MeasurementSeries((MeasurementPoint(plan.batch_size, tuple(samples)),), label)
 
 
 def time_workload_phases(program, state, plan, order, repeats: int = 10, *, dtype="f64",
                          devices=None, build: str = "manual", pdl: bool = False,
-                         while_loop: bool = False, meminfo: bool = False) -> dict:
+                         while_loop: bool = False, meminfo: bool = False, fuse: bool = False) -> dict:
     """Per-repeat samples split into the paper's phases.
 
     Returns {"creation": [T_C...], "execution": [T_E...], "total": [...], "gpu": [device T_E...],
@@ -741,7 +741,7 @@ def time_workload_phases(program, state, plan, order, repeats: int = 10, *, dtyp
     if reps < 1:
         raise ValueError("repeats must be >= 1")
     _check_program(program, state)
-    s = _solver_for(state, dtype, devices)
+    s = _solver_for(state, dtype, devices, fuse)
     out = {"creation": [], "execution": [], "total": [], "gpu": [], "times": []}
     batched = _order_value(order) == ExecutionOrder.BATCHED.value
     for r in range(reps):

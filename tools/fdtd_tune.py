@@ -7,9 +7,10 @@ n = int(os.environ.get("N", "256"))
 st = cli.build_workload("fdtd", [n])
 variants = [("two-kernel staged (default)", False, {}), ("two-kernel lean", False, {"IB_FDTD_KERNEL": "lean"}),
             ("fused default", True, {})]
-for tj, ns, chunks in ((4, 6, 0), (4, 5, 0), (3, 4, 0), (2, 5, 0), (3, 6, 0), (4, 6, 1)):
-    variants.append((f"two-kernel tj={tj} ns={ns} chunks={chunks}", False,
-                     {"IB_FDTD_TJ": tj, "IB_FDTD_STAGES": ns, "IB_FDTD_CHUNKS": chunks}))
+for fuse in (True, False):
+    for tj, ns in ((4, 6), (6, 4), (6, 3), (8, 3), (3, 4)):
+        variants.append((f"{'fused' if fuse else 'two-kernel'} tj={tj} ns={ns}", fuse,
+                         {"IB_FDTD_TJ": tj, "IB_FDTD_STAGES": ns}))
 for name, fuse, env in variants:
     for k in ("IB_FDTD_TJ", "IB_FDTD_STAGES", "IB_FDTD_CTAS", "IB_FDTD_CHUNKS", "IB_FDTD_TILES", "IB_FDTD_KERNEL"):
         os.environ.pop(k, None)

@@ -3,11 +3,13 @@ import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl
 
-KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES")
+KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES", "IB_HOTSPOT_RB")
 cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
 variants = [("auto", {})]
-for r in (1, 2, 4):
+for r in (1, 2):
     variants.append((f"vec R={r}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r}))
+for rb in (1, 2, 4, 8):
+    variants.append((f"tile RB={rb}", {"IB_HOTSPOT_KERNEL": "tile", "IB_HOTSPOT_RB": rb}))
 if os.environ.get("ALL"):
     for rpc in (2, 4, 8, 16):
         variants.append((f"tma rpc={rpc}", {"IB_HOTSPOT_KERNEL": "tma", "IB_HOTSPOT_RPC": rpc}))

@@ -29,7 +29,8 @@ from iterbatch.optimize import recommend_from_coefficients  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CONFIGS = [("skeleton", 10000, "vector 2^14"), ("skeleton_pdl", 10000, "vector 2^14, PDL edges"),
            ("hotspot2d", 10000, "Hotspot2D 1024^2"), ("hotspot3d", 1000, "Hotspot3D 512x512x8"),
-           ("fdtd", 2000, "FDTD 256^3 (2 kernels / iteration)")]
+           ("fdtd", 2000, "FDTD 256^3 (2 kernels / iteration)"),
+           ("fdtd_fused", 2000, "FDTD 256^3 fused (1 kernel / iteration)")]
 
 
 def main():
