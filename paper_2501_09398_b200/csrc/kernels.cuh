@@ -176,8 +176,9 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // y-row). grid = (ceil(M/V/256), ceil(rows/R)).
 // Measured alternatives that were not faster in-graph (Hotspot2D 1024^2 / Hotspot3D 512^2x8):
 // 2-D CTAs sharing x rows through L1, 2-4 warp-strided groups per thread (fewer instructions per
-// cell), a whole y-row per thread: the one-wave kernel is bound by its memory round trip and the
-// L1/TEX request rate, and fewer, fatter threads expose more latency.
+// cell), a whole y-row per thread, a shared-memory tile staging the x rows once per CTA (+40%:
+// the barrier serialises the load and compute rounds): the one-wave kernel is bound by its
+// memory round trip, and fewer, fatter or synchronised threads expose more latency.
 // ================================================================================================
 template <typename T, bool D3, int R>
 __global__ void __launch_bounds__(256)
@@ -249,94 +250,6 @@ __global__ void __launch_bounds__(256)
     if (i == 0 && halo_up) st16<T>(halo_up + m, out);
     if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
   }
-}
-
-// ================================================================================================
-// Hotspot, shared-memory tile variant for L2-resident grids. A CTA owns RB consecutive rows of a
-// strip of S = (256/RB)*V plane cells; it loads the RB+2 x-rows of the strip plus a y-halo of H
-// cells each side (H = L in 3-D, V in 2-D) into shared memory ONCE (L2 reads of T: (RB+2)/RB
-// instead of 3), then each thread computes one 16-byte group of one row from shared memory.
-// Edge clamps: x rows by clamped row index, the strip's y-halo beyond the plane by clamped cell
-// index (np.pad "edge": the clamped neighbour is the edge cell itself), z in 3-D by a per-thread
-// select (l == 0 / l == L-1). grid = (ceil(M / S), ceil(rows / RB)), dynamic smem
-// (RB+2)*(S+2H)*sizeof(T).
-// ================================================================================================
-template <typename T, bool D3, int RB>
-__global__ void __launch_bounds__(256)
-    k_hotspot_tile(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power, int rows,
-                   int C, int L, T k, T loss, int has_top, int has_bot, T *__restrict__ halo_up,
-                   T *__restrict__ halo_dn) {
-  constexpr int V = 16 / sizeof(T);
-  constexpr int W = 256 / RB;  // groups per strip row
-  constexpr int S = W * V;     // cells per strip row
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T *tile = reinterpret_cast<T *>(smem_raw);
-  pdl_trigger();
-  const int M = C * L;
-  const int H = D3 ? L : V;
-  const int SW = S + 2 * H;  // tile row width
-  const int m0 = blockIdx.x * S, i0 = blockIdx.y * RB;
-  const int tid = threadIdx.x, r = tid / W, g = tid - r * W;
-  const int m = m0 + g * V, i = i0 + r;
-  const bool mine = m < M && i < rows;
-  const int qlo = has_top ? -1 : 0, qhi = has_bot ? rows : rows - 1;
-  T pw[V];
-  if (mine) ld16<T>(pw, power + i * M + m);  // never written by a step: load before the wait
-  pdl_wait();
-  // ---- stage rows i0-1 .. i0+RB of cells [m0-H, m0+S+H) ---------------------------------------
-  const int gpr = SW / V;  // 16-byte groups per tile row
-  for (int idx = tid; idx < (RB + 2) * gpr; idx += 256) {
-    const int q0 = idx / gpr, cg = idx - q0 * gpr;
-    int q = i0 - 1 + q0;
-    q = q < qlo ? qlo : (q > qhi ? qhi : q);
-    const int mm = m0 - H + cg * V;
-    T v[V];
-    if (mm >= 0 && mm + V <= M) {
-      ld16<T>(v, src + q * M + mm);
-    } else {  // the strip's y-halo beyond the plane: clamp each cell (3-D: j to [0, C-1])
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        int c = mm + e;
-        if (D3) c = c < 0 ? c + L * ((-c + L - 1) / L) : (c >= M ? c - L * ((c - M) / L + 1) : c);
-        else c = c < 0 ? 0 : (c >= M ? M - 1 : c);
-        c = c < 0 ? 0 : (c >= M ? M - 1 : c);
-        v[e] = src[q * M + c];
-      }
-    }
-    st16<T>(tile + q0 * SW + cg * V, v);
-  }
-  __syncthreads();
-  if (!mine) return;
-  const T *t1 = tile + (r + 1) * SW + H + g * V;  // my row, my group
-  T up[V], c[V], dn[V], out[V];
-  ld16<T>(up, t1 - SW);
-  ld16<T>(c, t1);
-  ld16<T>(dn, t1 + SW);
-  if (D3) {
-    T ym[V], yp[V];
-    ld16<T>(ym, t1 - L);
-    ld16<T>(yp, t1 + L);
-    const int l = m % L;
-    const T zl = l > 0 ? t1[-1] : c[0];
-    const T zr = l + V < L ? t1[V] : c[V - 1];
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const T zm = e > 0 ? c[e - 1] : zl;
-      const T zp = e < V - 1 ? c[e + 1] : zr;
-      out[e] = hotspot_cell<T, true>(up[e], c[e], dn[e], ym[e], yp[e], zm, zp, pw[e], k, loss);
-    }
-  } else {
-    const T yl = t1[-1], yr = t1[V];  // the halo holds the clamped edge values
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const T a = e > 0 ? c[e - 1] : yl;
-      const T b = e < V - 1 ? c[e + 1] : yr;
-      out[e] = hotspot_cell<T, false>(up[e], c[e], dn[e], a, b, T(0), T(0), pw[e], k, loss);
-    }
-  }
-  st16<T>(dst + i * M + m, out);
-  if (i == 0 && halo_up) st16<T>(halo_up + m, out);
-  if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
 }
 
 // ---- bulk-copy (TMA) + mbarrier primitives ------------------------------------------------------
@@ -636,9 +549,9 @@ __global__ void __launch_bounds__(256)
 // refilled. Masks are branch-free selects; a run starting at x0 > 0 first recomputes H_new(x0-1)
 // without writing, to seed the carry.
 // ================================================================================================
-constexpr int kLfMaxThreads = 640;  // (TJ+1) x groups-per-row threads, rounded up to warps
-// TJ <= 4: up to 384 threads, two CTAs per SM must fit the register file; TJ 6 / 8: one CTA per SM
-constexpr int lf_max_threads(int tj) { return tj <= 4 ? 384 : 640; }
+// (TJ+1) x groups-per-row threads, rounded up to warps; two CTAs per SM must fit the register file.
+// (TJ = 6 / 8 with one CTA per SM measured no faster than TJ = 4: 141.6 / 212.9 vs 142.6 us fused.)
+constexpr int kLfMaxThreads = 384;
 // MODE: kLfFused (above), kLfH / kLfE = the H or the E half-step alone, in place (src == dst),
 // the two-launch leapfrog of the reference's program (workloads.py:325-413). Same staging and
 // march; H alone skips the seed plane and the E phase, E alone loads H instead of computing it and
@@ -648,7 +561,7 @@ constexpr int lf_max_threads(int tj) { return tj <= 4 ? 384 : 640; }
 constexpr int kLfFused = 0, kLfH = 1, kLfE = 2;
 
 template <typename T, bool UNIT_D, int TJ, int MODE>
-__global__ void __launch_bounds__(ib::lf_max_threads(TJ), TJ <= 4 ? 2 : 1)
+__global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
     k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int tiles, int chunks,
               int nstages, T c_h, T c_e, T d) {
   extern __shared__ __align__(128) unsigned char smem_raw[];

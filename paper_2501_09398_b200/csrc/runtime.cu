@@ -324,7 +324,7 @@ int hotspot_rows_per_chunk(const ib_ctx *c, int rows) {
 //   vec    one 16-byte group per thread, every load independent: best for L2-resident grids
 //   tma    cp.async.bulk plane-march pipeline: best once the state no longer fits in L2
 //   scalar marching fallback for shapes the vector paths cannot take (M or L not a multiple of V)
-enum class HotKernel { Scalar, Vec, Tma, Tile };
+enum class HotKernel { Scalar, Vec, Tma };
 
 template <typename T>
 int tma_groups(const ib_ctx *c) {  // G such that TM = G*V*256 holds whole y-rows; 0 = not possible
@@ -349,7 +349,6 @@ HotKernel hotspot_variant(const ib_ctx *c, int rows) {
   const bool tma_ok = vec_ok && tma_groups<T>(c) > 0 && rows >= 2;
   const char *force = env_str("IB_HOTSPOT_KERNEL");
   if (force) {
-    if (!std::strcmp(force, "tile") && vec_ok && (!d3 || L <= 256)) return HotKernel::Tile;
     if (!std::strcmp(force, "tma") && tma_ok) return HotKernel::Tma;
     if (!std::strcmp(force, "vec") && vec_ok) return HotKernel::Vec;
     if (!std::strcmp(force, "scalar")) return HotKernel::Scalar;
@@ -368,15 +367,6 @@ const void *tma_fn(int G) {
     default: return (const void *)ib::k_hotspot_tma<T, D3, 2>;
   }
 }
-
-template <typename T, bool D3>
-const void *tile_fn_d(int RB) {
-  return RB >= 8 ? (const void *)ib::k_hotspot_tile<T, D3, 8>
-         : RB == 4 ? (const void *)ib::k_hotspot_tile<T, D3, 4>
-         : RB == 2 ? (const void *)ib::k_hotspot_tile<T, D3, 2> : (const void *)ib::k_hotspot_tile<T, D3, 1>;
-}
-template <typename T>
-const void *tile_fn(bool d3, int RB) { return d3 ? tile_fn_d<T, true>(RB) : tile_fn_d<T, false>(RB); }
 
 template <typename T>
 void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
@@ -433,20 +423,6 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         dim3 grid((unsigned)xblocks, (unsigned)((rows + R - 1) / R));
         out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, k, loss,
                                   top, bot, up, dn));
-        break;
-      }
-      case HotKernel::Tile: {
-        int64_t RB = env_int("IB_HOTSPOT_RB", 4);
-        RB = RB >= 8 ? 8 : RB >= 4 ? 4 : RB >= 2 ? 2 : 1;
-        const int64_t S = (256 / RB) * V, H = d3 ? L : V;
-        const size_t smem = (size_t)(RB + 2) * (S + 2 * H) * sizeof(T);
-        const void *fn = tile_fn<T>(d3, (int)RB);
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        dim3 grid((unsigned)((plane + S - 1) / S), (unsigned)((rows + RB - 1) / RB));
-        Launch Lt = make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, k, loss, top,
-                                bot, up, dn);
-        Lt.smem = smem;
-        out.push_back(Lt);
         break;
       }
       case HotKernel::Tma: {
@@ -507,11 +483,10 @@ inline LfConfig lf_config(const ib_ctx *c) {
   LfConfig cfg;
   const int64_t ftj = env_int("IB_FDTD_TJ", 0), fns = env_int("IB_FDTD_STAGES", 0);
   const struct { int tj; bool two; } order[] = {{4, false}, {3, true}, {4, true}, {2, true},
-                                                 {3, false}, {2, false}, {1, true}, {1, false},
-                                                 {6, false}, {8, false}};
+                                                 {3, false}, {2, false}, {1, true}, {1, false}};
   for (auto o : order) {
     if (ftj > 0 && o.tj != ftj) continue;
-    if (lf_threads(c, o.tj) > ib::lf_max_threads(o.tj)) continue;
+    if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
     for (int ns = 3; ns <= 8; ++ns) {
       if (fns > 0 && ns != fns) continue;
       const size_t sm = lf_smem(o.tj, ns, P, es);
@@ -523,7 +498,7 @@ inline LfConfig lf_config(const ib_ctx *c) {
   }
   if (!cfg.tj) {  // nothing deep enough: take any shape that fits
     for (auto o : order) {
-      if (lf_threads(c, o.tj) > ib::lf_max_threads(o.tj)) continue;
+      if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
       const size_t sm = lf_smem(o.tj, 3, P, es);
       if (sm <= cap) { cfg = {o.tj, 3, sm}; break; }
     }
@@ -537,8 +512,6 @@ const void *lf_fn_m(int tj) {
     case 1: return (const void *)ib::k_fdtd_lf<T, U, 1, M>;
     case 2: return (const void *)ib::k_fdtd_lf<T, U, 2, M>;
     case 3: return (const void *)ib::k_fdtd_lf<T, U, 3, M>;
-    case 6: return (const void *)ib::k_fdtd_lf<T, U, 6, M>;
-    case 8: return (const void *)ib::k_fdtd_lf<T, U, 8, M>;
     default: return (const void *)ib::k_fdtd_lf<T, U, 4, M>;
   }
 }

@@ -43,7 +43,7 @@ HOT_SHAPES = [(64, 48), (33, 1024), (7, 4100), (1, 8), (40, 12, 8), (9, 20, 256)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("kernel", ["scalar", "vec", "tma", "tile"])
+@pytest.mark.parametrize("kernel", ["scalar", "vec", "tma"])
 @pytest.mark.parametrize("shape", HOT_SHAPES, ids=["x".join(map(str, s)) for s in HOT_SHAPES])
 def test_hotspot_variant_bitwise(gpu, env, shape, kernel, dtype):
     env(IB_HOTSPOT_KERNEL=kernel)
@@ -69,21 +69,6 @@ def test_hotspot_tma_chunking_and_ring_depth(gpu, env, rpc, stages):
         assert np.array_equal(np.asarray(got, np.float32), want), shape
 
 
-@pytest.mark.parametrize("rb", [1, 2, 4, 8])
-def test_hotspot_tile_rows_per_cta(gpu, env, rb):
-    """The shared-memory tile kernel for every rows-per-CTA choice: strip y-halos clamped at the
-    plane edges, partial strips and row chunks, z clamps at every y-row edge."""
-    env(IB_HOTSPOT_KERNEL="tile", IB_HOTSPOT_RB=rb)
-    rng = np.random.default_rng(rb)
-    for shape in ((23, 16, 8), (30, 5, 4), (9, 3, 16), (7, 40, 64), (5, 2, 256), (31, 64), (6, 8),
-                  (11, 1000), (3, 5000), (2, 1, 4)):
-        for dtype, npd in (("f32", np.float32), ("f64", np.float64)):
-            state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
-            want = ocpu.hotspot(state.temperature, state.power, 0.1, 5, npd)
-            got = wl.run_batched(wl.hotspot_program(), state, 5, 1, dtype=dtype, pdl=True).temperature
-            assert np.array_equal(np.asarray(got, npd), want), (shape, dtype)
-
-
 @pytest.mark.parametrize("rows", [1, 2, 4])
 def test_hotspot_vec_rows_per_thread(gpu, env, rows):
     """The vectorised kernel with every rows-per-thread choice, ragged last row chunk included."""
@@ -97,7 +82,7 @@ def test_hotspot_vec_rows_per_thread(gpu, env, rows):
             assert np.array_equal(np.asarray(got, npd), want), (shape, dtype)
 
 
-@pytest.mark.parametrize("kernel", ["vec", "tma", "scalar", "tile"])
+@pytest.mark.parametrize("kernel", ["vec", "tma", "scalar"])
 @pytest.mark.parametrize("slabs", [2, 3, 5])
 def test_hotspot_variants_with_slabs(gpu, env, kernel, slabs):
     env(IB_HOTSPOT_KERNEL=kernel, IB_HOTSPOT_RPC=3)

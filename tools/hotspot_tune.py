@@ -8,8 +8,7 @@ cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
 variants = [("auto", {})]
 for r in (1, 2):
     variants.append((f"vec R={r}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r}))
-for rb in (1, 2, 4, 8):
-    variants.append((f"tile RB={rb}", {"IB_HOTSPOT_KERNEL": "tile", "IB_HOTSPOT_RB": rb}))
+
 if os.environ.get("ALL"):
     for rpc in (2, 4, 8, 16):
         variants.append((f"tma rpc={rpc}", {"IB_HOTSPOT_KERNEL": "tma", "IB_HOTSPOT_RPC": rpc}))

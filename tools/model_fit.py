@@ -78,7 +78,7 @@ def main():
         out += ["## Measured timeline constants (CUPTI trace, `python -m paper_2501_09398_b200 trace`)", "",
                 "Medians over one traced graph run (K = 100) and one traced stream run; µs. Observation I "
                 "of the paper (`PAPER.md:208`) holds when t_i < t_a.", "",
-                "| config | t_k | t_i (in-graph gap) | t_a (between graphs) | t_b (stream gap) | t_l | k_c | b_c |",
+                "| config | t_k | t_i (in-graph gap) | t_a (between graphs) | t_b (stream gap) | t_l (incl. CUPTI first-launch setup) | k_c | b_c |",
                 "|---|---|---|---|---|---|---|---|"] + traces
     path = os.path.join(ROOT, "profiles", f"{a.round}_model_fit.md")
     with open(path, "w") as fh:
