@@ -546,7 +546,11 @@ __global__ void __launch_bounds__(256)
 //   phase E (rows r >= 1): E_new(i) from E_old(i) and H_new(i) (own registers; row j-1 and
 //            column k-1 from the ring) and H_new(i-1) hy/hz carried in registers.
 // The barrier of plane t also proves every thread is done with plane t-1's stage, which is then
-// refilled. Masks are branch-free selects; a run starting at x0 > 0 first recomputes H_new(x0-1)
+// refilled. A launch covers planes [x0, x0 + npl) (global indices; src / dst are pre-offset so
+// global plane indices address the buffer): the whole lattice, or one axis-0 slab of it. Slabs
+// (two half-step solver): the H launch also stores its last plane's H into the next slab's halo
+// plane (halo_h), the E launch its first plane's E into the previous slab's (halo_e) — device-
+// local or peer pointers; ordering is the launch layer's cross-slab graph edges. Masks are branch-free selects; a run starting at x0 > 0 first recomputes H_new(x0-1)
 // without writing, to seed the carry.
 // ================================================================================================
 // (TJ+1) x groups-per-row threads, rounded up to warps; two CTAs per SM must fit the register file.
@@ -562,8 +566,9 @@ constexpr int kLfFused = 0, kLfH = 1, kLfE = 2;
 
 template <typename T, bool UNIT_D, int TJ, int MODE>
 __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
-    k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int tiles, int chunks,
-              int nstages, T c_h, T c_e, T d) {
+    k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int x0, int npl, int tiles,
+              int chunks, int nstages, T c_h, T c_e, T d, T *halo_h, int64_t fs_h, T *halo_e,
+              int64_t fs_e) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int V = 16 / sizeof(T);
   constexpr int ER = TJ + 2, HR = TJ + 1;  // E rows / H rows per stage
@@ -574,7 +579,7 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
   const int tid = threadIdx.x;
   const int G = P / V;
   const int r = tid / G, k0 = (tid - r * G) * V;
-  const int ny1 = ny + 1, nxp = nx + 1;
+  const int ny1 = ny + 1, nxp = npl;  // this launch's planes: [x0, x0 + npl) (global indices)
   int64_t u_begin, u_end;
   if (chunks > 0) {  // lockstep: CTA = (tile, x-chunk), equal chunk bounds for every tile
     const int tile = blockIdx.x / chunks, ch = blockIdx.x - tile * chunks;
@@ -603,8 +608,8 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
   uint32_t g_base = 0;  // stage uses so far (mbarrier phase bookkeeping across runs)
   for (int64_t u = u_begin; u < u_end;) {
     const int tile = (int)(u / nxp);
-    const int i0 = (int)(u - (int64_t)tile * nxp);
-    const int i1 = (int)min((int64_t)nxp, (int64_t)i0 + (u_end - u));
+    const int i0 = x0 + (int)(u - (int64_t)tile * nxp);
+    const int i1 = x0 + (int)min((int64_t)nxp, (int64_t)(i0 - x0) + (u_end - u));
     u += i1 - i0;
     // tile rows [j0, j0 + h), h <= TJ: the (ny+1) rows split evenly over `tiles` tiles
     const int j0 = (int)((int64_t)(ny + 1) * tile / tiles);
@@ -699,6 +704,12 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
           st16<T>(o + 3 * FS, hx);
           st16<T>(o + 4 * FS, hy);
           st16<T>(o + 5 * FS, hz);
+          if (halo_h && i == x0 + npl - 1) {  // slabs: my last plane -> the next slab's H halo
+            T *q = halo_h + (int64_t)jj * P + k0;
+            st16<T>(q + 3 * fs_h, hx);
+            st16<T>(q + 4 * fs_h, hy);
+            st16<T>(q + 5 * fs_h, hz);
+          }
         }
       }
       __syncthreads();  // H_new(i) complete in the ring; plane t-1's stage is free
@@ -728,6 +739,12 @@ __global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
           st16<T>(o, ex);
           st16<T>(o + FS, ey);
           st16<T>(o + 2 * FS, ez);
+          if (halo_e && i == x0) {  // slabs: my first plane -> the previous slab's E halo
+            T *q = halo_e + (int64_t)jj * P + k0;
+            st16<T>(q, ex);
+            st16<T>(q + fs_e, ey);
+            st16<T>(q + 2 * fs_e, ez);
+          }
         }
 #pragma unroll
         for (int e = 0; e < V; ++e) {

@@ -72,6 +72,7 @@ struct Launch {
   dim3 grid, block;
   size_t smem = 0;  // dynamic shared memory bytes
   int slab = 0;
+  int step = 0;  // half-step index within an iteration (FDTD: 0 = H, 1 = E) for cross-slab ordering
   int nargs = 0;
   static constexpr int kMaxArgs = 24;
   alignas(16) unsigned char slot[kMaxArgs][16];
@@ -113,6 +114,7 @@ struct Slab {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // "iteration t done" double buffer for neighbours
   cudaEvent_t join = nullptr;              // fork/join of the slab streams
+  int64_t fs = 0;  // FDTD slabs: lattice field stride (elements) of buf[0]
   int rows() const { return row_hi - row_lo; }
 };
 
@@ -526,7 +528,8 @@ const void *lf_fn(bool unit, int tj, int mode) {
 // One k_fdtd_lf launch of `mode` from lattice buffer `from` to `to` (equal for the in-place
 // half-steps).
 template <typename T>
-Launch lf_launch(ib_ctx *c, int mode, void *from, void *to) {
+Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int64_t fs, void *halo_h = nullptr,
+                 int64_t fs_h = 0, void *halo_e = nullptr, int64_t fs_e = 0, int slab = 0) {
   const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
   const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
   const bool unit = c->scalars[0] == 1.0;
@@ -546,17 +549,19 @@ Launch lf_launch(ib_ctx *c, int mode, void *from, void *to) {
   if (env_int("IB_FDTD_TILES", 0) >= min_tiles) tiles = std::min<int64_t>(ny + 1, env_int("IB_FDTD_TILES", 0));
   int64_t chunks = env_int("IB_FDTD_CHUNKS", 0);
   if (chunks <= 0) chunks = std::max<int64_t>(1, slots / tiles);
-  chunks = std::min<int64_t>(chunks, nx + 1);  // every chunk non-empty
+  chunks = std::min<int64_t>(chunks, npl);  // every chunk non-empty
   int64_t ctas = env_int("IB_FDTD_CTAS", 0);
   if (ctas <= 0) {
     ctas = tiles * chunks;  // one CTA per (tile, chunk): the kernel maps blockIdx.x to both
   } else {
     chunks = 0;  // even split of the tile-major unit list over `ctas` CTAs
-    ctas = std::max<int64_t>(1, std::min(ctas, tiles * (nx + 1)));
+    ctas = std::max<int64_t>(1, std::min(ctas, tiles * npl));
   }
-  Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), 0, (const T *)from, (T *)to, nx,
-                         ny, nz, (int)c->lat_pitch, c->lat_fs, (int)tiles, (int)chunks, cfg.ns, ch, ce, d);
+  Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), slab, (const T *)from, (T *)to, nx,
+                         ny, nz, (int)c->lat_pitch, fs, x0, npl, (int)tiles, (int)chunks, cfg.ns, ch, ce, d,
+                         (T *)halo_h, fs_h, (T *)halo_e, fs_e);
   L.smem = cfg.smem;
+  L.step = mode == ib::kLfE ? 1 : 0;
   return L;
 }
 
@@ -567,12 +572,36 @@ template <typename T>
 void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   const char *force = env_str("IB_FDTD_KERNEL");
   const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0;
-  if (!lean) {
-    out.push_back(lf_launch<T>(c, ib::kLfH, c->lat[0], c->lat[0]));
-    out.push_back(lf_launch<T>(c, ib::kLfE, c->lat[0], c->lat[0]));
+  const int nx = (int)c->dims[0];
+  const int P = (int)c->slabs.size();
+  if (P > 1) {  // axis-0 slabs: every H launch, then every E launch, halo planes pushed in-kernel
+    const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lat_pitch;
+    for (int step = 0; step < 2; ++step)
+      for (int g = 0; g < P; ++g) {
+        Slab &s = c->slabs[g];
+        T *base = (T *)s.buf[0] + (int64_t)(1 - s.row_lo) * plane;  // global plane index -> buffer
+        void *hh = nullptr, *he = nullptr;
+        int64_t fh = 0, fe = 0;
+        if (step == 0 && g + 1 < P) {
+          hh = c->slabs[g + 1].buf[0];  // its top halo plane (local 0)
+          fh = c->slabs[g + 1].fs;
+        }
+        if (step == 1 && g > 0) {
+          Slab &n = c->slabs[g - 1];
+          he = (T *)n.buf[0] + (int64_t)(n.rows() + 1) * plane;  // its bottom halo plane
+          fe = n.fs;
+        }
+        out.push_back(lf_launch<T>(c, step == 0 ? ib::kLfH : ib::kLfE, base, base, s.row_lo, s.rows(), s.fs,
+                                   hh, fh, he, fe, g));
+      }
     return;
   }
-  const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
+  if (!lean) {
+    out.push_back(lf_launch<T>(c, ib::kLfH, c->lat[0], c->lat[0], 0, nx + 1, c->lat_fs));
+    out.push_back(lf_launch<T>(c, ib::kLfE, c->lat[0], c->lat[0], 0, nx + 1, c->lat_fs));
+    return;
+  }
+  const int ny = (int)c->dims[1], nz = (int)c->dims[2];
   const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
   const bool unit = c->scalars[0] == 1.0;
   dim3 b2(32, 8);
@@ -582,12 +611,14 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   T *f = (T *)c->lat[0];
   out.push_back(make_launch(fh, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ch, d));
   out.push_back(make_launch(fe, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ce, d));
+  out.back().step = 1;
 }
 
 // FDTD fused: one k_fdtd_lf launch per iteration, parity -> parity ^ 1.
 template <typename T>
 void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
-  out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1]));
+  out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1], 0, (int)c->dims[0] + 1,
+                             c->lat_fs));
 }
 
 void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
@@ -696,6 +727,8 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
   iteration_launches(c, 0, its[0]);
   if (c->ping_pong()) iteration_launches(c, 1, its[1]);
   const int P = (int)c->slabs.size();
+  int steps = 1;  // half-steps per iteration (launches are listed step-major)
+  for (const Launch &L : its[0]) steps = std::max(steps, L.step + 1);
   int par = parity;
   int64_t nk = 0;
   for (int64_t t = 0; t < iters; ++t) {
@@ -704,11 +737,14 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
       Launch &L = v[q];
       Slab &s = c->slabs[L.slab];
       cudaStream_t st = (P == 1 && single_stream) ? single_stream : s.stream;
+      // phase = global half-step index; a slab's launch of phase f waits for its neighbours'
+      // launches of phase f-1 (RAW on the halo it reads, WAR on the halo it writes)
+      const int64_t f = t * steps + L.step;
       if (P > 1) {
         IB_CUDA(cudaSetDevice(s.device));
-        if (t > 0) {
-          if (L.slab > 0) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab - 1].ev[(t - 1) & 1], 0));
-          if (L.slab + 1 < P) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab + 1].ev[(t - 1) & 1], 0));
+        if (f > 0) {
+          if (L.slab > 0) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab - 1].ev[(f - 1) & 1], 0));
+          if (L.slab + 1 < P) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab + 1].ev[(f - 1) & 1], 0));
         }
       }
       // PDL only chains kernels on the same stream; the very first launch has no predecessor.
@@ -718,7 +754,7 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
       c->ev(single_stream ? IB_EV_NODE_ADDED : IB_EV_BASELINE_KERNEL_LAUNCHED, single_stream ? -1 : t,
             single_stream ? nk : (int64_t)q);
       IB_TRY(launch_one(L, st, use_pdl));
-      if (P > 1) IB_CUDA(cudaEventRecord(s.ev[t & 1], st));
+      if (P > 1) IB_CUDA(cudaEventRecord(s.ev[f & 1], st));
       ++nk;
     }
     if (c->dist()) {  // boundary planes of this iteration's output <-> neighbouring ranks
@@ -1002,8 +1038,10 @@ void ib_destroy(ib_ctx *c) {
 static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   const int P = ndevices;
   const bool hot = c->solver == IB_SOLVER_HOTSPOT2D || c->solver == IB_SOLVER_HOTSPOT3D;
-  if (P > 1 && !hot) return fail(IB_EINVAL, "multi-slab execution is only defined for hotspot solvers");
-  const int64_t rows = hot ? c->dims[0] : 1;
+  if (P > 1 && !hot && c->solver != IB_SOLVER_FDTD)
+    return fail(IB_EINVAL, "multi-slab execution is defined for the hotspot solvers and the two-half-step FDTD");
+  // axis-0 slabs: hotspot rows, or the FDTD lattice's nx+1 planes
+  const int64_t rows = hot ? c->dims[0] : (c->solver == IB_SOLVER_FDTD && P > 1 ? c->dims[0] + 1 : 1);
   if (P > rows) return fail(IB_EINVAL, "more slabs than rows along axis 0");
   c->slabs.resize(P);
   const bool dist = c->nranks > 1;
@@ -1070,6 +1108,21 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
     const bool fused = c->solver == IB_SOLVER_FDTD_FUSED;
     if (fused && lf_config(c).tj == 0)
       return fail(IB_EINVAL, "fused fdtd: the z rows are too long for one CTA (threads or shared-memory ring); use the two-kernel solver");
+    if (P > 1) {  // slabs: each owns planes [lo, hi) plus one halo plane each side, in place
+      if (lf_config(c).tj == 0)
+        return fail(IB_EINVAL, "fdtd slabs need the staged kernel: the z rows are too long for one CTA");
+      const int64_t plane = (ny + 1) * c->lat_pitch;
+      for (Slab &s : c->slabs) {
+        IB_CUDA(cudaSetDevice(s.device));
+        s.fs = (int64_t)(s.rows() + 2) * plane;
+        const size_t bb = (size_t)(6 * s.fs * es);
+        IB_CUDA(cudaMalloc(&s.buf[0], bb));
+        IB_CUDA(cudaMemset(s.buf[0], 0, bb));
+      }
+      IB_CUDA(cudaSetDevice(c->slabs[0].device));
+      IB_CUDA(cudaDeviceSynchronize());
+      return IB_OK;
+    }
     const size_t b = (size_t)(6 * c->lat_fs * es);
     for (int p = 0; p < (fused ? 2 : 1); ++p) {
       IB_CUDA(cudaMalloc(&c->lat[p], b));
@@ -1370,6 +1423,33 @@ static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
   DeviceGuard guard;
   if (c->hotspot()) return hotspot_copy(c, field, host, bytes, up);
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  if (c->fdtd() && c->slabs.size() > 1) {  // slabs: owned planes (+ halo planes on upload)
+    const int64_t *sh = c->fshape[field];
+    const size_t es = (size_t)c->esize;
+    const int64_t plane = (c->dims[1] + 1) * c->lat_pitch;
+    for (Slab &s : c->slabs) {
+      IB_CUDA(cudaSetDevice(s.device));
+      const int64_t lo = up ? std::max<int64_t>(s.row_lo - 1, 0) : s.row_lo;
+      const int64_t hi = std::min<int64_t>(up ? s.row_hi + 1 : s.row_hi, sh[0]);  // this field's planes
+      if (hi <= lo) continue;
+      char *hbase = (char *)host + (size_t)(lo * sh[1] * sh[2]) * es;
+      char *dbase = (char *)s.buf[0] + (size_t)(field * s.fs + (lo - s.row_lo + 1) * plane) * es;
+      cudaMemcpy3DParms m = {};
+      cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, (size_t)sh[2] * es, (size_t)sh[2] * es, (size_t)sh[1]);
+      cudaPitchedPtr dp = make_cudaPitchedPtr(dbase, (size_t)c->lat_pitch * es, (size_t)sh[2] * es,
+                                              (size_t)(c->dims[1] + 1));
+      m.srcPtr = up ? hp : dp;
+      m.dstPtr = up ? dp : hp;
+      m.extent = make_cudaExtent((size_t)sh[2] * es, (size_t)sh[1], (size_t)(hi - lo));
+      m.kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+      IB_CUDA(cudaMemcpy3DAsync(&m, s.stream));
+    }
+    for (Slab &s : c->slabs) {
+      IB_CUDA(cudaSetDevice(s.device));
+      IB_CUDA(cudaStreamSynchronize(s.stream));
+    }
+    return IB_OK;
+  }
   void *dev = c->fieldp(field, c->cur);
   if (c->fdtd()) {  // C-order host array <-> padded lattice
     const int64_t *sh = c->fshape[field];
@@ -1464,7 +1544,7 @@ int ib_run_step(ib_ctx *c, int step, ib_times *tm) {
   IB_CUDA(cudaEventRecord(c->t0, c->stream()));
   IB_TRY(join_into(c, c->stream(), true));
   for (Launch &L : v) {
-    if (c->solver == IB_SOLVER_FDTD && &L != &v[step]) continue;
+    if (c->solver == IB_SOLVER_FDTD && L.step != step) continue;
     Slab &s = c->slabs[L.slab];
     IB_CUDA(cudaSetDevice(s.device));
     IB_TRY(launch_one(L, s.stream, false));
@@ -1546,7 +1626,7 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
   if (!c->exec[c->cur]) IB_TRY(build_one(c, c->cur, &t));
   if (c->ping_pong() && (c->K & 1) && !c->exec[c->cur ^ 1]) IB_TRY(build_one(c, c->cur ^ 1, &t));
   const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
-  const int64_t per = c->K * (c->solver == IB_SOLVER_FDTD ? 2 : (int64_t)c->slabs.size());  // kernels / batch
+  const int64_t per = c->K * (c->solver == IB_SOLVER_FDTD ? 2 : 1) * (int64_t)c->slabs.size();  // kernels / batch
   auto a = clk::now();
   IB_CUDA(cudaEventRecord(c->t0, c->stream()));
   if (num_batches > 0) {

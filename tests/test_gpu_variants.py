@@ -192,3 +192,32 @@ def test_fdtd_fused_non_unit_cell_size(gpu, env, ctas):
         got = wl.run_loop(wl.fdtd_program(), w, 9, dtype=dtype, fuse=True)
         for g, ww in zip(got.state_arrays(), want):
             assert np.array_equal(np.asarray(g, npd), ww)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("slabs", [2, 3, 5])
+@pytest.mark.parametrize("dims", [(8, 4, 8), (16, 9, 33), (5, 6, 7), (40, 9, 70)],
+                         ids=["8x4x8", "16x9x33", "5x6x7", "40x9x70"])
+def test_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
+    """FDTD split into axis-0 slabs of the lattice (halo planes pushed by the H / E launches
+    into the neighbours, cross-slab graph edges) == one domain == the oracle, bit for bit, in
+    graph (capture) and stream mode, with tile / chunk variants."""
+    if slabs > dims[0] + 1:
+        pytest.skip("more slabs than planes")
+    base = wl.fdtd_cavity(*dims)
+    rng = np.random.default_rng(sum(dims) + slabs)
+    state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
+                            base.cell_size, base.time_step)
+    npd = np.float32 if dtype == "f32" else np.float64
+    dt = state.time_step
+    want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
+                     dt / wl.VACUUM_PERMITTIVITY, 6, npd)
+    devs = [0] * slabs
+    for tj, chunks in ((0, 0), (1, 2), (3, 1)):
+        env(IB_FDTD_TJ=tj, IB_FDTD_CHUNKS=chunks)
+        got = wl.run_batched(wl.fdtd_program(), state, 3, 2, dtype=dtype, devices=devs, build="capture")
+        for g, w in zip(got.state_arrays(), want):
+            assert np.array_equal(np.asarray(g, npd), w), (tj, chunks)
+        got = wl.run_loop(wl.fdtd_program(), state, 6, dtype=dtype, devices=devs)
+        for g, w in zip(got.state_arrays(), want):
+            assert np.array_equal(np.asarray(g, npd), w), (tj, chunks)
