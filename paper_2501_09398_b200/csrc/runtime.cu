@@ -270,8 +270,10 @@ struct ib_ctx {
   void *peer_buf_up[2] = {nullptr, nullptr}, *peer_buf_dn[2] = {nullptr, nullptr};
   unsigned long long *peer_sync_up = nullptr, *peer_sync_dn = nullptr;
   int peer_rows_up = 0;  // the up neighbour's owned rows (locates its bottom halo plane)
+  int peer_rows_dn = 0;  // the down neighbour's (FDTD: its lattice field stride)
   bool peer = false;
   bool dist() const { return nranks > 1; }
+  int64_t lattice_pitch() const { return lat_pitch; }
   // tracing (CUPTI activity records; host events on the CUPTI timebase)
   bool tracing = false;
   int64_t trace_cap = 0;
@@ -574,6 +576,24 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0;
   const int nx = (int)c->dims[0];
   const int P = (int)c->slabs.size();
+  if (c->dist()) {  // one rank's slab; the neighbours' halo planes through IPC mappings
+    const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lattice_pitch();
+    Slab &s = c->slabs[0];
+    T *base = (T *)s.buf[0] + (int64_t)(1 - s.row_lo) * plane;
+    void *hh = nullptr, *he = nullptr;
+    int64_t fh = 0, fe = 0;
+    if (c->peer && s.has_bot) {
+      hh = c->peer_buf_dn[0];  // the down rank's top halo plane (its local 0)
+      fh = (int64_t)(c->peer_rows_dn + 2) * plane;
+    }
+    if (c->peer && s.has_top) {
+      he = (T *)c->peer_buf_up[0] + (int64_t)(c->peer_rows_up + 1) * plane;  // the up rank's bottom halo
+      fe = (int64_t)(c->peer_rows_up + 2) * plane;
+    }
+    out.push_back(lf_launch<T>(c, ib::kLfH, base, base, s.row_lo, s.rows(), s.fs, hh, fh, nullptr, 0, 0));
+    out.push_back(lf_launch<T>(c, ib::kLfE, base, base, s.row_lo, s.rows(), s.fs, nullptr, 0, he, fe, 0));
+    return;
+  }
   if (P > 1) {  // axis-0 slabs: every H launch, then every E launch, halo planes pushed in-kernel
     const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lat_pitch;
     for (int step = 0; step < 2; ++step)
@@ -750,20 +770,17 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
       // PDL only chains kernels on the same stream; the very first launch has no predecessor.
       // Peer-exchange contexts never use it: the wait / signal kernels must not overlap the stencil.
       const bool use_pdl = pdl && P == 1 && (t > 0 || q > 0) && !c->peer;
-      if (c->peer && q == 0) IB_TRY(launch_dist_wait(c, st));
+      if (c->peer) IB_TRY(launch_dist_wait(c, st));  // neighbours done with the previous phase
       c->ev(single_stream ? IB_EV_NODE_ADDED : IB_EV_BASELINE_KERNEL_LAUNCHED, single_stream ? -1 : t,
             single_stream ? nk : (int64_t)q);
       IB_TRY(launch_one(L, st, use_pdl));
       if (P > 1) IB_CUDA(cudaEventRecord(s.ev[f & 1], st));
+      if (c->peer) IB_TRY(launch_dist_signal(c, st));  // its halo planes went out with its stores
       ++nk;
     }
     if (c->dist()) {  // boundary planes of this iteration's output <-> neighbouring ranks
       cudaStream_t st = single_stream ? single_stream : c->slabs[0].stream;
-      if (c->peer) {
-        IB_TRY(launch_dist_signal(c, st));  // the halo planes went out with the kernel's stores
-      } else {
-        IB_TRY(nccl_exchange(c, par ^ 1, st));
-      }
+      if (!c->peer) IB_TRY(nccl_exchange(c, par ^ 1, st));
     }
     if (c->ping_pong()) par ^= 1;
   }
@@ -1041,11 +1058,12 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   if (P > 1 && !hot && c->solver != IB_SOLVER_FDTD)
     return fail(IB_EINVAL, "multi-slab execution is defined for the hotspot solvers and the two-half-step FDTD");
   // axis-0 slabs: hotspot rows, or the FDTD lattice's nx+1 planes
-  const int64_t rows = hot ? c->dims[0] : (c->solver == IB_SOLVER_FDTD && P > 1 ? c->dims[0] + 1 : 1);
+  const int64_t rows = hot ? c->dims[0] : (c->solver == IB_SOLVER_FDTD && (P > 1 || c->nranks > 1) ? c->dims[0] + 1 : 1);
   if (P > rows) return fail(IB_EINVAL, "more slabs than rows along axis 0");
   c->slabs.resize(P);
   const bool dist = c->nranks > 1;
-  if (dist && (P != 1 || !hot)) return fail(IB_EINVAL, "distributed contexts are single-slab hotspot grids");
+  if (dist && (P != 1 || !(hot || c->solver == IB_SOLVER_FDTD)))
+    return fail(IB_EINVAL, "distributed contexts are single-slab hotspot or two-half-step FDTD grids");
   if (dist && c->nranks > rows) return fail(IB_EINVAL, "more ranks than rows along axis 0");
   for (int g = 0; g < P; ++g) {
     Slab &s = c->slabs[g];
@@ -1108,7 +1126,7 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
     const bool fused = c->solver == IB_SOLVER_FDTD_FUSED;
     if (fused && lf_config(c).tj == 0)
       return fail(IB_EINVAL, "fused fdtd: the z rows are too long for one CTA (threads or shared-memory ring); use the two-kernel solver");
-    if (P > 1) {  // slabs: each owns planes [lo, hi) plus one halo plane each side, in place
+    if (P > 1 || dist) {  // slabs / ranks: planes [lo, hi) plus one halo plane each side, in place
       if (lf_config(c).tj == 0)
         return fail(IB_EINVAL, "fdtd slabs need the staged kernel: the z rows are too long for one CTA");
       const int64_t plane = (ny + 1) * c->lat_pitch;
@@ -1262,9 +1280,11 @@ int ib_nccl_unique_id(void *id128) {
 int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
                    const double *scalars, int nscalars, int device, int rank, int nranks,
                    const void *id128) {
-  if (solver != IB_SOLVER_HOTSPOT2D && solver != IB_SOLVER_HOTSPOT3D)
-    return fail(IB_EINVAL, "distributed contexts are defined for hotspot grids");
+  if (solver != IB_SOLVER_HOTSPOT2D && solver != IB_SOLVER_HOTSPOT3D && solver != IB_SOLVER_FDTD)
+    return fail(IB_EINVAL, "distributed contexts are defined for hotspot grids and the two-half-step FDTD");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(IB_EINVAL, "bad rank / nranks");
+  if (solver == IB_SOLVER_FDTD && nranks > 1 && id128)
+    return fail(IB_EINVAL, "distributed FDTD uses the peer exchange: pass id128 = NULL, then ib_ipc_attach");
 
   return create_common(out, solver, dtype, dims, ndims, scalars, nscalars, &device, 1, rank, nranks,
                        id128);
@@ -1277,7 +1297,9 @@ int ib_ipc_export(const ib_ctx *c, void *out, size_t bytes) {
   DeviceGuard guard;
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
   cudaIpcMemHandle_t h[3];
-  for (int p = 0; p < 2; ++p) IB_CUDA(cudaIpcGetMemHandle(&h[p], c->slabs[0].buf[p]));
+  std::memset(h, 0, sizeof(h));
+  for (int p = 0; p < 2; ++p)
+    if (c->slabs[0].buf[p]) IB_CUDA(cudaIpcGetMemHandle(&h[p], c->slabs[0].buf[p]));  // FDTD: one lattice
   IB_CUDA(cudaIpcGetMemHandle(&h[2], c->sync));
   std::memcpy(out, h, sizeof(h));
   return IB_OK;
@@ -1295,7 +1317,7 @@ int ib_ipc_attach(ib_ctx *c, const void *up, const void *dn) {
   auto open = [&](const void *blob, void **bufs, unsigned long long **sync) -> int {
     cudaIpcMemHandle_t h[3];
     std::memcpy(h, blob, sizeof(h));
-    for (int p = 0; p < 2; ++p)
+    for (int p = 0; p < (c->fdtd() ? 1 : 2); ++p)
       IB_CUDA(cudaIpcOpenMemHandle(&bufs[p], h[p], cudaIpcMemLazyEnablePeerAccess));
     void *sp = nullptr;
     IB_CUDA(cudaIpcOpenMemHandle(&sp, h[2], cudaIpcMemLazyEnablePeerAccess));
@@ -1304,8 +1326,9 @@ int ib_ipc_attach(ib_ctx *c, const void *up, const void *dn) {
   };
   if (s.has_top) IB_TRY(open(up, c->peer_buf_up, &c->peer_sync_up));
   if (s.has_bot) IB_TRY(open(dn, c->peer_buf_dn, &c->peer_sync_dn));
-  const int64_t rows = c->dims[0];
+  const int64_t rows = c->fdtd() ? c->dims[0] + 1 : c->dims[0];
   c->peer_rows_up = (int)(rows * c->rank / c->nranks - rows * (c->rank - 1) / c->nranks);
+  c->peer_rows_dn = (int)(rows * (c->rank + 2) / c->nranks - rows * (c->rank + 1) / c->nranks);
   c->peer = true;
   return IB_OK;
 }
@@ -1313,8 +1336,9 @@ int ib_ipc_attach(ib_ctx *c, const void *up, const void *dn) {
 int ib_slab_info(const ib_ctx *c, int64_t *lo, int64_t *hi, int *has_top, int *has_bot) {
   IB_TRY(check_ctx(c));
   const Slab &s = c->slabs[0];
-  if (lo) *lo = c->hotspot() ? s.row_lo : 0;
-  if (hi) *hi = c->hotspot() ? s.row_hi : c->dims[0];
+  const bool sl = c->hotspot() || (c->fdtd() && c->dist());
+  if (lo) *lo = sl ? s.row_lo : 0;
+  if (hi) *hi = sl ? s.row_hi : c->dims[0];
   if (has_top) *has_top = c->nranks > 1 && s.has_top;
   if (has_bot) *has_bot = c->nranks > 1 && s.has_bot;
   return IB_OK;
@@ -1407,15 +1431,28 @@ static int hotspot_copy(ib_ctx *c, int field, void *host, size_t bytes, bool up)
   return IB_OK;
 }
 
+// FDTD slab / rank: the global planes of `field` a transfer moves — upload: the owned planes and
+// the halo plane each side that exists, download: the owned planes; clipped to the field's extent.
+static void fdtd_planes(const ib_ctx *c, const Slab &s, int field, bool up, int64_t *lo, int64_t *hi) {
+  const int64_t n = c->fshape[field][0];
+  *lo = std::min<int64_t>(up ? std::max<int64_t>(s.row_lo - 1, 0) : s.row_lo, n);
+  *hi = std::min<int64_t>(up ? s.row_hi + 1 : s.row_hi, n);
+  if (*hi < *lo) *hi = *lo;
+}
+
 static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
   IB_TRY(check_ctx(c));
   if (field < 0 || field >= c->nfields) return fail(IB_EINVAL, "field index out of range");
   if (!host) return fail(IB_EINVAL, "host pointer is null");
   int64_t want = ib_field_bytes(c, field);
-  if (c->nranks > 1) {
+  if (c->nranks > 1 && c->hotspot()) {
     const Slab &s = c->slabs[0];
     const int64_t pb = c->plane() * c->esize;
     want = (field == 0 && up) ? (s.rows() + s.has_top + s.has_bot) * pb : s.rows() * pb;
+  } else if (c->nranks > 1) {  // FDTD rank: this field's planes of the window (see the header)
+    int64_t lo, hi;
+    fdtd_planes(c, c->slabs[0], field, up, &lo, &hi);
+    want = (hi - lo) * c->fshape[field][1] * c->fshape[field][2] * c->esize;
   }
   if ((int64_t)bytes != want)
     return fail(IB_EINVAL, "field " + std::to_string(field) + " holds " + std::to_string(want) +
@@ -1423,16 +1460,21 @@ static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
   DeviceGuard guard;
   if (c->hotspot()) return hotspot_copy(c, field, host, bytes, up);
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
-  if (c->fdtd() && c->slabs.size() > 1) {  // slabs: owned planes (+ halo planes on upload)
+  if (c->fdtd() && (c->slabs.size() > 1 || c->dist())) {  // slabs / ranks: owned (+ halo) planes
     const int64_t *sh = c->fshape[field];
     const size_t es = (size_t)c->esize;
     const int64_t plane = (c->dims[1] + 1) * c->lat_pitch;
+    int64_t host0 = 0;  // global plane of the host buffer's first plane (a rank holds its window)
+    if (c->dist()) {
+      int64_t hi0;
+      fdtd_planes(c, c->slabs[0], field, up, &host0, &hi0);
+    }
     for (Slab &s : c->slabs) {
       IB_CUDA(cudaSetDevice(s.device));
-      const int64_t lo = up ? std::max<int64_t>(s.row_lo - 1, 0) : s.row_lo;
-      const int64_t hi = std::min<int64_t>(up ? s.row_hi + 1 : s.row_hi, sh[0]);  // this field's planes
+      int64_t lo, hi;
+      fdtd_planes(c, s, field, up, &lo, &hi);
       if (hi <= lo) continue;
-      char *hbase = (char *)host + (size_t)(lo * sh[1] * sh[2]) * es;
+      char *hbase = (char *)host + (size_t)((lo - host0) * sh[1] * sh[2]) * es;
       char *dbase = (char *)s.buf[0] + (size_t)(field * s.fs + (lo - s.row_lo + 1) * plane) * es;
       cudaMemcpy3DParms m = {};
       cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, (size_t)sh[2] * es, (size_t)sh[2] * es, (size_t)sh[1]);

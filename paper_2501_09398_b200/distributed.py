@@ -101,15 +101,18 @@ class DistributedSolver(DeviceSolver):
     def __init__(self, state, dtype, rank: int, world: int, device: int, uid: bytes | None = None,
                  upload: bool = True, exchange: str = "nccl", allgather=None):
         kind = _kind_of_state(state)
-        if kind not in ("hotspot2d", "hotspot3d"):
-            raise ValueError("distributed execution is defined for hotspot grids")
+        if kind not in ("hotspot2d", "hotspot3d", "fdtd"):
+            raise ValueError("distributed execution is defined for hotspot grids and FDTD")
+        if kind == "fdtd" and world > 1 and exchange != "peer":
+            raise ValueError("distributed FDTD uses exchange='peer'")
         self.kind = kind
         self.dtype = _norm_dtype(dtype)
         self.np_dtype = _NP_DTYPE[self.dtype]
         self.dims, self.scalars = _dims_scalars(kind, state)
         self.devices = (device,)
         self.rank, self.world = rank, world
-        self.rows = self.dims[0]
+        # axis-0 units: hotspot rows, FDTD lattice planes (nx + 1)
+        self.rows = self.dims[0] + (1 if kind == "fdtd" else 0)
         self.lo, self.hi = slab_bounds(self.rows, world, rank)
         self.wlo, self.whi = halo_window(self.rows, world, rank)
         L = _lib.lib()
@@ -132,9 +135,21 @@ class DistributedSolver(DeviceSolver):
         self._ctx = ctx
         if world > 1 and exchange == "peer":
             self._attach_peers(allgather)
-        self.nfields = 2
-        plane = tuple(self.dims[1:])
-        self.shapes = [(self.hi - self.lo,) + plane, (self.hi - self.lo,) + plane]
+        if kind == "fdtd":
+            self.nfields = 6
+            self.field_shapes = []
+            for f in range(6):
+                shp = (ctypes.c_int64 * 3)()
+                nd = ctypes.c_int()
+                _lib.check(L.ib_field_shape(ctx, f, shp, ctypes.byref(nd)))
+                self.field_shapes.append(tuple(shp[:3]))
+            # download: owned planes [lo, hi) of each field, clipped to its extent (the header)
+            self.shapes = [(max(0, min(self.hi, fs[0]) - min(self.lo, fs[0])),) + fs[1:]
+                           for fs in self.field_shapes]
+        else:
+            self.nfields = 2
+            plane = tuple(self.dims[1:])
+            self.shapes = [(self.hi - self.lo,) + plane, (self.hi - self.lo,) + plane]
         self.batch_size = 0
         if upload:
             self.upload(state)
@@ -179,6 +194,12 @@ class DistributedSolver(DeviceSolver):
         return solver
 
     def host_arrays(self, state):
+        if self.kind == "fdtd":  # every field's window: [lo - top, hi + bot) clipped to its extent
+            out = []
+            for a, fs in zip(state.state_arrays(), self.field_shapes):
+                lo, hi = min(self.wlo, fs[0]), min(self.whi, fs[0])
+                out.append(np.ascontiguousarray(a[lo:hi], dtype=self.np_dtype))
+            return out
         t = np.ascontiguousarray(state.temperature[self.wlo:self.whi], dtype=self.np_dtype)
         p = np.ascontiguousarray(state.power[self.lo:self.hi], dtype=self.np_dtype)
         return [t, p]
@@ -205,6 +226,13 @@ class DistributedSolver(DeviceSolver):
         """This rank's owned rows [lo, hi) of the current temperature."""
         return self.download_field(0)
 
+    def local_fields(self) -> list[np.ndarray]:
+        """FDTD: this rank's owned planes [lo, hi) of every field (clipped to each extent)."""
+        return [self.download_field(f) for f in range(self.nfields)]
+
     @property
     def iteration_bytes(self) -> int:
+        if self.kind == "fdtd":  # this rank's share of the global H + E half-step bytes
+            g = int(_lib.lib().ib_iteration_bytes(self.ctx))
+            return g * (self.hi - self.lo) // self.rows
         return 3 * int(np.prod(self.shapes[0])) * np.dtype(self.np_dtype).itemsize
