@@ -43,7 +43,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 //             rounding c=0.9999 to binary32 drifts 1.7e-4 over 10^4 steps; this form 2.5e-6).
 // Launch: one float4 / double2 per thread; a scalar tail handles n % 4 (n % 2).
 // ================================================================================================
-__global__ void __launch_bounds__(256) k_vector_f32(float *__restrict__ v, int64_t n, double c) {
+__global__ void __launch_bounds__(1024) k_vector_f32(float *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_vector_f32(float *__restrict__ v, int64
   }
 }
 
-__global__ void __launch_bounds__(256) k_vector_f64(double *__restrict__ v, int64_t n, double c) {
+__global__ void __launch_bounds__(1024) k_vector_f64(double *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -173,7 +173,10 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // itself — so the per-row work is 5 loads, 1 store and the cell arithmetic, with 32-bit offsets
 // (the launch layer checks the slab buffer holds < 2^31 elements).
 // Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles a
-// y-row). grid = (ceil(M/V/256), ceil(rows/R)).
+// y-row). block = (bx groups of a row, by row-blocks), 256 threads by default: an EMPTY kernel's
+// per-launch floor in a PDL graph falls with fewer, bigger CTAs (1024 x 256 threads 1.41 us,
+// 256 x 1024 0.57 us, tools/microbench_floor.cu), but this kernel measured slower with 512- and
+// 1024-thread CTAs — a CTA retires at its slowest warp. grid = (ceil(M/V/bx), ceil(rows/(R*by))).
 // Measured alternatives that were not faster in-graph (Hotspot2D 1024^2 / Hotspot3D 512^2x8):
 // 2-D CTAs sharing x rows through L1, 2-4 warp-strided groups per thread (fewer instructions per
 // cell), a whole y-row per thread, a shared-memory tile staging the x rows once per CTA (+40%:
@@ -181,7 +184,7 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // memory round trip, and fewer, fatter or synchronised threads expose more latency.
 // ================================================================================================
 template <typename T, bool D3, int R>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     k_hotspot_vec(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
                   int rows, int C, int L, T k, T loss, int has_top, int has_bot,
                   T *__restrict__ halo_up, T *__restrict__ halo_dn) {
@@ -189,8 +192,8 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();
   const int M = C * L;
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) * V;
-  const int i0 = blockIdx.y * R;
-  if (m >= M) return;
+  const int i0 = (blockIdx.y * blockDim.y + threadIdx.y) * R;
+  if (m >= M || i0 >= rows) return;
   const int nr = min(R, rows - i0);
   // neighbour offsets relative to the group's first cell, edge-clamped once
   int oym, oyp, ozl, ozr;  // y-1 / y+1 group, z-1 / z+1 scalar (3-D); 2-D: y is the row axis

@@ -412,11 +412,19 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         // R=4 4.67; Hotspot2D 1024^2 R=1 2.56, R=2 3.12. IB_HOTSPOT_VEC_ROWS overrides.
         int64_t R = env_int("IB_HOTSPOT_VEC_ROWS", 0);
         const int64_t threads_per_row = plane / V;
-        const int64_t xblocks = (threads_per_row + 255) / 256;
+        // CTA shape: bx threads along a plane row (up to 256), by row-blocks, bx*by = IB_HOTSPOT_BLOCK.
+        // 256 measured best in-graph (Hotspot3D 512^2x8: 4.45 / 4.79 / 6.20 us at 256 / 512 / 1024;
+        // Hotspot2D 2.60 / 2.65 / 2.68) although an EMPTY kernel's launch floor falls with fewer,
+        // bigger CTAs (tools/microbench_floor.cu): real CTAs retire at their slowest warp.
+        int64_t bs = env_int("IB_HOTSPOT_BLOCK", 256);
+        bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
+        const int64_t bx = std::min<int64_t>(std::min<int64_t>(256, bs), (threads_per_row + 31) / 32 * 32);
+        const int64_t by = std::max<int64_t>(1, bs / bx);
+        const int64_t xblocks = (threads_per_row + bx - 1) / bx;
         if (R <= 0) {
-          const int64_t slots = 6LL * c->num_sms;  // 256-thread CTAs at <= 40 registers
+          const int64_t slots = 1536LL * c->num_sms;  // resident threads at <= 40 registers
           R = 1;
-          while (R < 4 && xblocks * ((rows + R - 1) / R) > 4 * slots) R *= 2;
+          while (R < 4 && xblocks * bx * ((rows + R - 1) / R) > 4 * slots) R *= 2;
         }
         R = R >= 4 ? 4 : (R >= 2 ? 2 : 1);
         const void *fn;
@@ -424,8 +432,9 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
                    : R == 2 ? (const void *)ib::k_hotspot_vec<T, true, 2> : (const void *)ib::k_hotspot_vec<T, true, 1>;
         else fn = R == 4 ? (const void *)ib::k_hotspot_vec<T, false, 4>
                   : R == 2 ? (const void *)ib::k_hotspot_vec<T, false, 2> : (const void *)ib::k_hotspot_vec<T, false, 1>;
-        dim3 grid((unsigned)xblocks, (unsigned)((rows + R - 1) / R));
-        out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, k, loss,
+        dim3 grid((unsigned)xblocks, (unsigned)((rows + R * by - 1) / (R * by)));
+        out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)by), g, src, dst, (const T *)s.power,
+                                  rows, C, L, k, loss,
                                   top, bot, up, dn));
         break;
       }
@@ -647,14 +656,18 @@ void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     case IB_SOLVER_VECTOR: {
       const int64_t n = c->dims[0];
       const double cc = c->scalars[0];
+      // 128-thread CTAs measured best (1.21 / 1.23 / 1.24 / 1.40 us per iteration in a PDL graph at
+      // 128 / 256 / 512 / 1024); IB_VECTOR_BLOCK overrides
+      int64_t bs = env_int("IB_VECTOR_BLOCK", 128);
+      bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
       if (c->dtype == IB_F32) {
         const int64_t threads = (n >> 2) + (n & 3);
-        dim3 block(128), grid((unsigned)((threads + 127) / 128));
+        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
         out.push_back(make_launch((const void *)ib::k_vector_f32, grid, block, 0,
                                   (float *)c->field[0], n, cc));
       } else {
         const int64_t threads = (n >> 1) + (n & 1);
-        dim3 block(128), grid((unsigned)((threads + 127) / 128));
+        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
         out.push_back(make_launch((const void *)ib::k_vector_f64, grid, block, 0,
                                   (double *)c->field[0], n, cc));
       }

@@ -69,10 +69,11 @@ def test_hotspot_tma_chunking_and_ring_depth(gpu, env, rpc, stages):
         assert np.array_equal(np.asarray(got, np.float32), want), shape
 
 
-@pytest.mark.parametrize("rows", [1, 2, 4])
-def test_hotspot_vec_rows_per_thread(gpu, env, rows):
-    """The vectorised kernel with every rows-per-thread choice, ragged last row chunk included."""
-    env(IB_HOTSPOT_KERNEL="vec", IB_HOTSPOT_VEC_ROWS=rows)
+@pytest.mark.parametrize("rows,block", [(1, 256), (2, 256), (4, 256), (1, 1024), (2, 512), (4, 64)])
+def test_hotspot_vec_rows_per_thread(gpu, env, rows, block):
+    """The vectorised kernel with every rows-per-thread choice and 2-D CTA shapes (row-blocks
+    per CTA), ragged last row chunk and partially idle CTAs included."""
+    env(IB_HOTSPOT_KERNEL="vec", IB_HOTSPOT_VEC_ROWS=rows, IB_HOTSPOT_BLOCK=block)
     rng = np.random.default_rng(rows)
     for shape in ((23, 16, 8), (30, 5, 4), (9, 3, 16), (31, 64), (6, 8)):
         for dtype, npd in (("f32", np.float32), ("f64", np.float64)):

@@ -3,20 +3,24 @@ import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl
 
-KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES", "IB_HOTSPOT_RB")
-cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
+KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES", "IB_HOTSPOT_BLOCK",
+        "IB_VECTOR_BLOCK")
+cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000), ("vector", [16384], 2000)]
 variants = [("auto", {})]
 for r in (1, 2):
-    variants.append((f"vec R={r}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r}))
+    for bs in (256, 512, 1024):
+        variants.append((f"vec R={r} block={bs}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
+                                                   "IB_HOTSPOT_BLOCK": bs}))
 
 if os.environ.get("ALL"):
     for rpc in (2, 4, 8, 16):
         variants.append((f"tma rpc={rpc}", {"IB_HOTSPOT_KERNEL": "tma", "IB_HOTSPOT_RPC": rpc}))
     for rpc in (2, 4, 8):
         variants.append((f"scalar rpc={rpc}", {"IB_HOTSPOT_KERNEL": "scalar", "IB_HOTSPOT_RPC": rpc}))
+vec_variants = [(f"block={bs}", {"IB_VECTOR_BLOCK": bs}) for bs in (128, 256, 512, 1024)]
 for w, size, n in cfgs:
     st = cli.build_workload(w, size)
-    for name, env in variants:
+    for name, env in (vec_variants if w == "vector" else variants):
         for k in KEYS:
             os.environ.pop(k, None)
         os.environ.update({k: str(v) for k, v in env.items()})
