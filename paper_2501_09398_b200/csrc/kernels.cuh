@@ -183,7 +183,7 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // the barrier serialises the load and compute rounds): the one-wave kernel is bound by its
 // memory round trip, and fewer, fatter or synchronised threads expose more latency.
 // ================================================================================================
-template <typename T, bool D3, int R>
+template <typename T, bool D3, int R, int SH = 0>
 __global__ void __launch_bounds__(1024)
     k_hotspot_vec(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
                   int rows, int C, int L, T k, T loss, int has_top, int has_bot,
@@ -230,11 +230,43 @@ __global__ void __launch_bounds__(1024)
     const T *si = src + i * M + m;
     const T(&c)[V] = x[r + 1];
     T out[V];
-    const T zl = si[ozl], zr = si[ozr];
+    T zl, zr, ym[V], yp[V];
+    if (SH) {
+      // neighbours from the lanes that already hold them (a warp covers 32 consecutive groups of
+      // one row, whole y-rows of GL = L/V groups): z / row neighbours are lanes -+1, y rows
+      // lanes -+GL; only the warp's edge lanes load, edge clamps are selects
+      const unsigned FULL = 0xffffffffu;
+      const int lane = threadIdx.x & 31, GL = D3 ? L / V : 1;
+      const T up1 = __shfl_up_sync(FULL, c[V - 1], 1), dn1 = __shfl_down_sync(FULL, c[0], 1);
+      if (D3) {
+        const int g = lane % GL;  // group index within the y-row (l = g*V)
+        zl = g > 0 ? up1 : c[0];
+        zr = g < GL - 1 ? dn1 : c[V - 1];
+        if (SH == 2) {  // y rows too (measured slower at L = 8: 8 shuffles vs 2 loads)
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            ym[e] = __shfl_up_sync(FULL, c[e], GL);
+            yp[e] = __shfl_down_sync(FULL, c[e], GL);
+          }
+          if (lane < GL) ld16<T>(ym, si + oym);
+          if (lane >= 32 - GL) ld16<T>(yp, si + oyp);
+        } else {
+          ld16<T>(ym, si + oym);
+          ld16<T>(yp, si + oyp);
+        }
+      } else {
+        zl = lane > 0 ? up1 : si[ozl];
+        zr = lane < 31 ? dn1 : si[ozr];
+      }
+    } else {
+      zl = si[ozl];
+      zr = si[ozr];
+      if (D3) {
+        ld16<T>(ym, si + oym);
+        ld16<T>(yp, si + oyp);
+      }
+    }
     if (D3) {
-      T ym[V], yp[V];
-      ld16<T>(ym, si + oym);
-      ld16<T>(yp, si + oyp);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         const T zm = e > 0 ? c[e - 1] : zl;

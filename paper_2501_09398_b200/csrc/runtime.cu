@@ -372,6 +372,17 @@ const void *tma_fn(int G) {
   }
 }
 
+template <typename T, bool D3, int SH>
+const void *vec_fn_r(int R) {
+  return R >= 4 ? (const void *)ib::k_hotspot_vec<T, D3, 4, SH>
+                : R == 2 ? (const void *)ib::k_hotspot_vec<T, D3, 2, SH> : (const void *)ib::k_hotspot_vec<T, D3, 1, SH>;
+}
+template <typename T>
+const void *vec_fn(bool d3, int R, int sh) {
+  if (d3) return sh == 2 ? vec_fn_r<T, true, 2>(R) : sh == 1 ? vec_fn_r<T, true, 1>(R) : vec_fn_r<T, true, 0>(R);
+  return sh ? vec_fn_r<T, false, 1>(R) : vec_fn_r<T, false, 0>(R);
+}
+
 template <typename T>
 void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
   constexpr int V = 16 / sizeof(T);
@@ -406,10 +417,11 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     dim3 block(256);
     switch (hotspot_variant<T>(c, rows)) {
       case HotKernel::Vec: {
-        // rows per thread (R+2 row loads per R outputs): R = 1 (the most threads, the shortest
-        // per-thread chain) unless the grid would exceed four waves of resident CTAs. Measured
-        // in-graph with programmatic edges (us/iter): Hotspot3D 512x512x8 R=1 4.41, R=2 4.57,
-        // R=4 4.67; Hotspot2D 1024^2 R=1 2.56, R=2 3.12. IB_HOTSPOT_VEC_ROWS overrides.
+        // rows per thread (R+2 row loads per R outputs): with the neighbour loads (no shuffles)
+        // R = 1 — the most threads, the shortest per-thread chain — unless the grid would exceed
+        // four waves (measured: Hotspot3D 512x512x8 R=1 4.41, R=2 4.57, R=4 4.67 us/iter;
+        // Hotspot2D 1024^2 R=1 2.56, R=2 3.12); with shuffles R = 2 (below). IB_HOTSPOT_VEC_ROWS
+        // overrides.
         int64_t R = env_int("IB_HOTSPOT_VEC_ROWS", 0);
         const int64_t threads_per_row = plane / V;
         // CTA shape: bx threads along a plane row (up to 256), by row-blocks, bx*by = IB_HOTSPOT_BLOCK.
@@ -427,11 +439,16 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
           while (R < 4 && xblocks * bx * ((rows + R - 1) / R) > 4 * slots) R *= 2;
         }
         R = R >= 4 ? 4 : (R >= 2 ? 2 : 1);
-        const void *fn;
-        if (d3) fn = R == 4 ? (const void *)ib::k_hotspot_vec<T, true, 4>
-                   : R == 2 ? (const void *)ib::k_hotspot_vec<T, true, 2> : (const void *)ib::k_hotspot_vec<T, true, 1>;
-        else fn = R == 4 ? (const void *)ib::k_hotspot_vec<T, false, 4>
-                  : R == 2 ? (const void *)ib::k_hotspot_vec<T, false, 2> : (const void *)ib::k_hotspot_vec<T, false, 1>;
+        // warp shuffles for the in-row (2-D) / z (3-D) neighbours when every warp covers 32 groups
+        // of one row and whole y-rows: 1 = those, 2 = also the y rows. IB_HOTSPOT_SHUFFLE overrides.
+        const int64_t gl = d3 ? L / V : 1;
+        // Measured in-graph with PDL (us/iter, two runs): Hotspot3D 512^2x8 R=1 4.47, R=1+sh1 4.36,
+        // R=2+sh1 4.22-4.25, sh2 (y rows by 8 shuffles) 4.60-4.77; Hotspot2D 1024^2 R=1 2.61,
+        // R=1+sh1 2.49, R=2+sh1 2.45. So z / row shuffles, and 2 rows per thread with them.
+        int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", 1);
+        if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
+        if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
+        const void *fn = vec_fn<T>(d3, (int)R, (int)std::min<int64_t>(sh, 2));
         dim3 grid((unsigned)xblocks, (unsigned)((rows + R * by - 1) / (R * by)));
         out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)by), g, src, dst, (const T *)s.power,
                                   rows, C, L, k, loss,

@@ -69,13 +69,16 @@ def test_hotspot_tma_chunking_and_ring_depth(gpu, env, rpc, stages):
         assert np.array_equal(np.asarray(got, np.float32), want), shape
 
 
+@pytest.mark.parametrize("shuffle", [0, 1, 2])
 @pytest.mark.parametrize("rows,block", [(1, 256), (2, 256), (4, 256), (1, 1024), (2, 512), (4, 64)])
-def test_hotspot_vec_rows_per_thread(gpu, env, rows, block):
+def test_hotspot_vec_rows_per_thread(gpu, env, rows, block, shuffle):
     """The vectorised kernel with every rows-per-thread choice and 2-D CTA shapes (row-blocks
     per CTA), ragged last row chunk and partially idle CTAs included."""
-    env(IB_HOTSPOT_KERNEL="vec", IB_HOTSPOT_VEC_ROWS=rows, IB_HOTSPOT_BLOCK=block)
+    env(IB_HOTSPOT_KERNEL="vec", IB_HOTSPOT_VEC_ROWS=rows, IB_HOTSPOT_BLOCK=block, IB_HOTSPOT_SHUFFLE=shuffle)
     rng = np.random.default_rng(rows)
-    for shape in ((23, 16, 8), (30, 5, 4), (9, 3, 16), (31, 64), (6, 8)):
+    # shapes with whole warps per row (the shuffle path: 32 groups of 4/2 cells) and without
+    for shape in ((23, 16, 8), (30, 5, 4), (9, 3, 16), (31, 64), (6, 8), (7, 64, 8), (5, 32, 16),
+                  (9, 128, 4), (6, 256), (4, 512, 32), (3, 3, 128), (11, 2048)):
         for dtype, npd in (("f32", np.float32), ("f64", np.float64)):
             state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
             want = ocpu.hotspot(state.temperature, state.power, 0.1, 5, npd)

@@ -4,13 +4,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl
 
 KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES", "IB_HOTSPOT_BLOCK",
-        "IB_VECTOR_BLOCK")
-cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000), ("vector", [16384], 2000)]
+        "IB_VECTOR_BLOCK", "IB_HOTSPOT_SHUFFLE")
+cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
 variants = [("auto", {})]
 for r in (1, 2):
-    for bs in (256, 512, 1024):
-        variants.append((f"vec R={r} block={bs}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
-                                                   "IB_HOTSPOT_BLOCK": bs}))
+    for shv in (0, 1, 2):
+        variants.append((f"vec R={r} shuffle={shv}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
+                                                      "IB_HOTSPOT_SHUFFLE": shv}))
 
 if os.environ.get("ALL"):
     for rpc in (2, 4, 8, 16):
