@@ -7,8 +7,8 @@ KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_ST
         "IB_VECTOR_BLOCK", "IB_HOTSPOT_SHUFFLE")
 cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
 variants = [("auto", {})]
-for r in (1, 2):
-    for shv in (0, 1, 2):
+for r in (1, 2, 4):
+    for shv in (0, 1):
         variants.append((f"vec R={r} shuffle={shv}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
                                                       "IB_HOTSPOT_SHUFFLE": shv}))
 
