@@ -450,18 +450,16 @@ __global__ void __launch_bounds__(256)
 }
 
 // ================================================================================================
-// FDTD Yee leapfrog, fields in place.  workloads.py:325-413
+// FDTD Yee leapfrog.  workloads.py:325-413
 // Shapes for (nx, ny, nz) cells:  ex (nx,ny+1,nz+1) ey (nx+1,ny,nz+1) ez (nx+1,ny+1,nz)
 //                                 hx (nx+1,ny,nz)   hy (nx,ny+1,nz)   hz (nx,ny,nz+1)
-// One thread per point of the unified (nx+1)(ny+1)(nz+1) lattice updates every component that
-// exists there. blockIdx.y is the x index; the (y,z) plane is flattened on blockIdx.x so a warp
-// walks contiguous z. Each update is  F = F + c * ((p - q)/d - (r - s)/d)  (App. A); /d is
-// skipped when d == 1 (x/1 == x exactly in IEEE arithmetic).
+// All six live on one (nx+1)(ny+1)P lattice (k_fdtd_lf comment); a point of the lattice updates
+// every component that exists there. Each update is  F = F + c * ((p - q)/d - (r - s)/d)
+// (App. A); /d is skipped when d == 1 (x/1 == x exactly in IEEE arithmetic).
 // H half-step (workloads.py:334-350): hx needs ey(k+1), ez(j+1); hy needs ez(i+1), ex(k+1);
 // hz needs ex(j+1), ey(i+1).
 // E half-step (workloads.py:372-412): interior update, tangential wall components written 0
 // (the reference's copy-then-zero, fused; equivalence in SURVEY.md App. B.3).
-// ================================================================================================
 // ================================================================================================
 // FDTD, lean lattice kernels (the fallback for z rows too long for k_fdtd_lf's CTA). One thread
 // per lattice point, block = (32 along z, 8 along y), grid = (z-tiles, y-tiles, nx+1); every

@@ -8,8 +8,8 @@ Same names, signatures, dataclasses, validation messages and error types as
 reference              here                                        device work
 =====================  ==========================================  ===============================
 vector_scale_step      workloads.py:97-105                         1 launch of k_vector
-hotspot_step           workloads.py:167-207                        1 launch of k_hotspot<2D|3D>
-fdtd_h_step/e_step     workloads.py:325-413                        1 launch of k_fdtd_h / k_fdtd_e
+hotspot_step           workloads.py:167-207                        1 launch of k_hotspot_vec/tma
+fdtd_h_step/e_step     workloads.py:325-413                        1 launch of k_fdtd_lf H / E mode
 run_loop               workloads.py:442-450 (Listing 1)            N launches from a C++ loop
 run_batched            workloads.py:453-471 (Listings 2/3)         K-iteration CUDA graph, I replays
 time_workload          workloads.py:479-505                        timed T_C + T_E per repeat
