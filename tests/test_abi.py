@@ -90,3 +90,18 @@ def test_create_validates_arguments_before_touching_a_device():
     bad = (ctypes.c_int64 * 2)(0, 4)
     assert L.ib_create(ctypes.byref(ctx), 1, 0, bad, 2, sc, 1, None, 0) == _lib.IB_EINVAL
     assert L.ib_graph_run(None, 1, None) == _lib.IB_EINVAL
+
+
+def test_plain_c_caller_compiles_and_links(tmp_path):
+    """examples/hotspot_c.c: the C ABI is usable from C alone (gcc, the header, the .so)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lib_dir = os.path.join(ROOT, "paper_2501_09398_b200")
+    out = tmp_path / "hotspot_c"
+    r = subprocess.run(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-o", str(out),
+                        os.path.join(ROOT, "examples", "hotspot_c.c"), "-L", lib_dir, "-literbatch_b200",
+                        f"-Wl,-rpath,{lib_dir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

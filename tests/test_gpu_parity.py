@@ -260,3 +260,32 @@ def test_p0_fused_fdtd_matches_reference(gpu, kat):
     n, k = kat["iterations"], kat["batch_size"]
     out = wl.run_batched(_program("fdtd"), state, k, n // k, fuse=True, pdl=True)
     assert f"{wl.state_checksum(out):016x}" == kat["checksum"]
+
+
+def test_plain_c_caller_runs_and_matches_python(gpu, tmp_path):
+    """examples/hotspot_c.c through the C ABI alone == the same run through the Python layer."""
+    import os
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_2501_09398_b200")
+    exe = tmp_path / "hotspot_c"
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(root, "include"), "-o", str(exe),
+                    os.path.join(root, "examples", "hotspot_c.c"), "-L", lib_dir, "-literbatch_b200",
+                    f"-Wl,-rpath,{lib_dir}"], check=True)
+    r = subprocess.run([str(exe), "64", "200", "20"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    t0 = float(r.stdout.strip().split("T[0]=")[1])
+    # the same inputs (the example's LCG) through the Python API
+    n, s = 64, 20240817
+    t = np.empty(n * n, np.float32)
+    for i in range(n * n):
+        s = (s * 1664525 + 1013904223) & 0xFFFFFFFF
+        t[i] = np.float32((s >> 8) / 16777216.0)
+    p = (t * np.float32(1e-3)).astype(np.float32)
+    st = wl.HotspotWorkload(t.reshape(n, n).astype(np.float64), p.reshape(n, n).astype(np.float64), 0.1)
+    got = wl.run_batched(wl.hotspot_program(), st, 20, 10, dtype="f32", pdl=True).temperature
+    assert abs(float(got[0, 0]) - t0) <= 1e-6 * max(1.0, abs(t0))
