@@ -1606,6 +1606,8 @@ int ib_num_steps(const ib_ctx *c) { return c ? (c->solver == IB_SOLVER_FDTD ? 2 
 int ib_run_step(ib_ctx *c, int step, ib_times *tm) {
   IB_TRY(check_ctx(c));
   if (step < 0 || step >= ib_num_steps(c)) return fail(IB_EINVAL, "step index out of range");
+  if (c->dist())
+    return fail(IB_EINVAL, "per-step calls are not defined for distributed contexts (use ib_run_stream)");
   DeviceGuard guard;
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
   IB_TRY(sync_all(c));
