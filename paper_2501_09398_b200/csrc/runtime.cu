@@ -428,7 +428,9 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         // 256 measured best in-graph (Hotspot3D 512^2x8: 4.45 / 4.79 / 6.20 us at 256 / 512 / 1024;
         // Hotspot2D 2.60 / 2.65 / 2.68) although an EMPTY kernel's launch floor falls with fewer,
         // bigger CTAs (tools/microbench_floor.cu): real CTAs retire at their slowest warp.
-        int64_t bs = env_int("IB_HOTSPOT_BLOCK", 256);
+        // With shuffles and R = 2 (below), 2-D measured best at 512 threads (256 x 2 row-blocks:
+        // 2.33 vs 2.43 us/iter at 256), 3-D at 256 (4.21; 512: 4.61).
+        int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? 256 : 512);
         bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
         const int64_t bx = std::min<int64_t>(std::min<int64_t>(256, bs), (threads_per_row + 31) / 32 * 32);
         const int64_t by = std::max<int64_t>(1, bs / bx);

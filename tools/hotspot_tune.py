@@ -8,9 +8,9 @@ KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_ST
 cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
 variants = [("auto", {})]
 for r in (1, 2, 4):
-    for shv in (0, 1):
-        variants.append((f"vec R={r} shuffle={shv}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
-                                                      "IB_HOTSPOT_SHUFFLE": shv}))
+    for bs in (128, 256, 512):
+        variants.append((f"vec R={r} sh=1 block={bs}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
+                                                        "IB_HOTSPOT_SHUFFLE": 1, "IB_HOTSPOT_BLOCK": bs}))
 
 if os.environ.get("ALL"):
     for rpc in (2, 4, 8, 16):
