@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <cupti_activity.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys, no-ops without a tool
 
 #include <mutex>
 
@@ -51,6 +52,12 @@ int fail(int code, const std::string &msg) {
     int rc_ = (expr);      \
     if (rc_ != IB_OK) return rc_; \
   } while (0)
+
+// NVTX range for the lifetime of a scope (the build / launch phases the paper times).
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 using clk = std::chrono::steady_clock;
 double secs(clk::time_point a, clk::time_point b) {
@@ -914,6 +921,7 @@ int build_one(ib_ctx *c, int parity, ib_times *tm) {
   const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
   const int P = (int)c->slabs.size();
   int64_t nodes = 0;
+  NvtxRange range("ib graph build (create + instantiate + upload)");
   c->ev(IB_EV_BUILD_STARTED);
   auto a = clk::now();
   cudaGraph_t g = nullptr;
@@ -1575,6 +1583,7 @@ static int sync_all(ib_ctx *c) {
 }
 
 int ib_run_stream(ib_ctx *c, int64_t iterations, int flags, ib_times *tm) {
+  NvtxRange range("ib stream run (per-kernel launches)");
   IB_TRY(check_ctx(c));
   if (c->dist() && !c->comm && !c->peer)
     return fail(IB_ESTATE, "distributed context without an exchange: call ib_ipc_attach first");
@@ -1691,6 +1700,7 @@ int ib_graph_build(ib_ctx *c, int64_t batch_size, int build_mode, int flags, ib_
 }
 
 int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
+  NvtxRange range("ib graph run (batch launches)");
   IB_TRY(check_ctx(c));
   if (num_batches < 0) return fail(IB_EINVAL, "num_batches must be >= 0");
   if (c->K < 1) return fail(IB_ESTATE, "no graph built: call ib_graph_build first");
