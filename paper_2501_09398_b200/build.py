@@ -8,6 +8,7 @@ with the gpurun snapshot (it is not gpurun-ignored), and the Python layer loads 
 
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -18,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libiterbatch_b200.so")
 SOURCES = [os.path.join(CSRC, "runtime.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "kernels.cuh"), os.path.join(ROOT, "include", "iterbatch_b200.h")]
+DEPS = SOURCES + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "iterbatch_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -11,1006 +11,11 @@
 //   _fill_slabs  workloads.py:60-69    -> axis-0 slab decomposition rows*g//P across devices,
 //                                          halo planes pushed by the stencil kernel itself
 // The state lives in HBM for the whole run; the boundary is crossed by ib_upload/ib_download.
-#include <cuda_runtime.h>
-#include <cupti_activity.h>
-#include <dlfcn.h>
-#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys, no-ops without a tool
 
-#include <mutex>
-
-#include <algorithm>
-#include <chrono>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <string>
-#include <vector>
-
-#include "../../include/iterbatch_b200.h"
-#include "kernels.cuh"
-
-namespace {
-
-thread_local std::string g_err;
-
-int fail(int code, const std::string &msg) {
-  g_err = msg;
-  return code;
-}
-
-#define IB_CUDA(call)                                                                           \
-  do {                                                                                          \
-    cudaError_t e_ = (call);                                                                    \
-    if (e_ != cudaSuccess) {                                                                    \
-      return fail(e_ == cudaErrorMemoryAllocation ? IB_ENOMEM : IB_ECUDA,                       \
-                  std::string(#call) + ": " + cudaGetErrorName(e_) + ": " + cudaGetErrorString(e_)); \
-    }                                                                                           \
-  } while (0)
-
-#define IB_TRY(expr)       \
-  do {                     \
-    int rc_ = (expr);      \
-    if (rc_ != IB_OK) return rc_; \
-  } while (0)
-
-// NVTX range for the lifetime of a scope (the build / launch phases the paper times).
-struct NvtxRange {
-  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
-  ~NvtxRange() { nvtxRangePop(); }
-};
-
-using clk = std::chrono::steady_clock;
-double secs(clk::time_point a, clk::time_point b) {
-  return std::chrono::duration<double>(b - a).count();
-}
-
-// Restores the caller's current device (torch and other libraries rely on it).
-struct DeviceGuard {
-  int saved = -1;
-  DeviceGuard() { cudaGetDevice(&saved); }
-  ~DeviceGuard() {
-    if (saved >= 0) cudaSetDevice(saved);
-  }
-};
-
-// A kernel launch with its argument values stored by value (graph nodes copy them at add time).
-struct Launch {
-  const void *func = nullptr;
-  dim3 grid, block;
-  size_t smem = 0;  // dynamic shared memory bytes
-  int slab = 0;
-  int step = 0;  // half-step index within an iteration (FDTD: 0 = H, 1 = E) for cross-slab ordering
-  int nargs = 0;
-  static constexpr int kMaxArgs = 24;
-  alignas(16) unsigned char slot[kMaxArgs][16];
-  void *ptr[kMaxArgs];
-  void **args() {
-    for (int i = 0; i < nargs; ++i) ptr[i] = slot[i];
-    return ptr;
-  }
-};
-
-template <typename A>
-void put_args(Launch &L, A a) {
-  static_assert(sizeof(A) <= 16, "kernel argument too large");
-  std::memcpy(L.slot[L.nargs++], &a, sizeof(A));
-}
-template <typename A, typename... R>
-void put_args(Launch &L, A a, R... rest) {
-  put_args(L, a);
-  put_args(L, rest...);
-}
-template <typename... Args>
-Launch make_launch(const void *func, dim3 grid, dim3 block, int slab, Args... args) {
-  static_assert(sizeof...(Args) <= Launch::kMaxArgs, "too many kernel arguments for Launch");
-  Launch L;
-  L.func = func;
-  L.grid = grid;
-  L.block = block;
-  L.slab = slab;
-  put_args(L, args...);
-  return L;
-}
-
-struct Slab {
-  int device = 0;
-  int row_lo = 0, row_hi = 0;  // global rows owned [lo, hi)
-  bool has_top = false, has_bot = false;
-  void *buf[2] = {nullptr, nullptr};  // (rows_local + 2) planes each: halo, owned..., halo
-  void *power = nullptr;              // rows_local planes
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev[2] = {nullptr, nullptr};  // "iteration t done" double buffer for neighbours
-  cudaEvent_t join = nullptr;              // fork/join of the slab streams
-  int64_t fs = 0;  // FDTD slabs: lattice field stride (elements) of buf[0]
-  int rows() const { return row_hi - row_lo; }
-};
-
-const char *env_str(const char *name) {
-  const char *v = std::getenv(name);
-  return (v && *v) ? v : nullptr;
-}
-
-int64_t env_int(const char *name, int64_t dflt) {
-  const char *v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  return std::strtoll(v, nullptr, 10);
-}
-
-// ---- NCCL, loaded at run time (no link dependency; the process may already hold torch's copy) --
-struct NcclId { char internal[128]; };
-struct Nccl {
-  bool ok = false;
-  std::string err;
-  int (*GetUniqueId)(NcclId *) = nullptr;
-  int (*CommInitRank)(void **, int, NcclId, int) = nullptr;
-  int (*CommDestroy)(void *) = nullptr;
-  int (*Send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
-  int (*Recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
-  int (*GroupStart)() = nullptr;
-  int (*GroupEnd)() = nullptr;
-  const char *(*GetErrorString)(int) = nullptr;
-};
-Nccl &nccl() {
-  static Nccl n = [] {
-    Nccl r;
-    // The copy the process already holds (torch's), else IB_NCCL_LIB (the Python layer points it
-    // at the wheel torch links against, so a later `import torch` finds a compatible NCCL), else
-    // the loader's default. RTLD_LOCAL: never interpose NCCL symbols on other libraries.
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    const char *path = std::getenv("IB_NCCL_LIB");
-    if (!h && path && *path) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
-    if (!h) {
-      r.err = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
-      return r;
-    }
-    r.GetUniqueId = (int (*)(NcclId *))dlsym(h, "ncclGetUniqueId");
-    r.CommInitRank = (int (*)(void **, int, NcclId, int))dlsym(h, "ncclCommInitRank");
-    r.CommDestroy = (int (*)(void *))dlsym(h, "ncclCommDestroy");
-    r.Send = (int (*)(const void *, size_t, int, int, void *, cudaStream_t))dlsym(h, "ncclSend");
-    r.Recv = (int (*)(void *, size_t, int, int, void *, cudaStream_t))dlsym(h, "ncclRecv");
-    r.GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
-    r.GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
-    r.GetErrorString = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
-    r.ok = r.GetUniqueId && r.CommInitRank && r.CommDestroy && r.Send && r.Recv && r.GroupStart &&
-           r.GroupEnd && r.GetErrorString;
-    if (!r.ok) r.err = "libnccl.so.2 lacks a required symbol";
-    return r;
-  }();
-  return n;
-}
-constexpr int kNcclInt8 = 0;  // ncclInt8: halo planes move as raw bytes
-
-// ---- CUPTI activity tracing, loaded at run time (what nsys uses; no in-kernel instrumentation) -
-struct Cupti {
-  bool ok = false;
-  std::string err;
-  CUptiResult (*RegisterCallbacks)(CUpti_BuffersCallbackRequestFunc, CUpti_BuffersCallbackCompleteFunc) = nullptr;
-  CUptiResult (*Enable)(CUpti_ActivityKind) = nullptr;
-  CUptiResult (*Disable)(CUpti_ActivityKind) = nullptr;
-  CUptiResult (*FlushAll)(uint32_t) = nullptr;
-  CUptiResult (*GetNextRecord)(uint8_t *, size_t, CUpti_Activity **) = nullptr;
-  CUptiResult (*GetTimestamp)(uint64_t *) = nullptr;
-  std::mutex mu;
-  std::vector<int64_t> kernels;  // (start, end) pairs of this library's solver kernels
-};
-Cupti &cupti() {
-  static Cupti *c = [] {
-    Cupti *r = new Cupti();
-    void *h = dlopen("libcupti.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libcupti.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) {
-      r->err = std::string("dlopen(libcupti) failed: ") + dlerror();
-      return r;
-    }
-    r->RegisterCallbacks = (decltype(r->RegisterCallbacks))dlsym(h, "cuptiActivityRegisterCallbacks");
-    r->Enable = (decltype(r->Enable))dlsym(h, "cuptiActivityEnable");
-    r->Disable = (decltype(r->Disable))dlsym(h, "cuptiActivityDisable");
-    r->FlushAll = (decltype(r->FlushAll))dlsym(h, "cuptiActivityFlushAll");
-    r->GetNextRecord = (decltype(r->GetNextRecord))dlsym(h, "cuptiActivityGetNextRecord");
-    r->GetTimestamp = (decltype(r->GetTimestamp))dlsym(h, "cuptiGetTimestamp");
-    r->ok = r->RegisterCallbacks && r->Enable && r->Disable && r->FlushAll && r->GetNextRecord &&
-            r->GetTimestamp;
-    if (!r->ok) r->err = "libcupti lacks a required symbol";
-    return r;
-  }();
-  return *c;
-}
-void CUPTIAPI cupti_buffer_requested(uint8_t **buffer, size_t *size, size_t *max_records) {
-  *size = 8u << 20;
-  *buffer = (uint8_t *)aligned_alloc(8, *size);
-  *max_records = 0;
-}
-void CUPTIAPI cupti_buffer_completed(CUcontext, uint32_t, uint8_t *buffer, size_t, size_t valid) {
-  Cupti &c = cupti();
-  CUpti_Activity *rec = nullptr;
-  std::lock_guard<std::mutex> lock(c.mu);
-  while (c.GetNextRecord(buffer, valid, &rec) == CUPTI_SUCCESS) {
-    if (rec->kind != CUPTI_ACTIVITY_KIND_CONCURRENT_KERNEL && rec->kind != CUPTI_ACTIVITY_KIND_KERNEL) continue;
-    const CUpti_ActivityKernel9 *k = (const CUpti_ActivityKernel9 *)rec;
-    const char *n = k->name ? k->name : "";
-    // the solver kernels live in namespace ib (mangled _ZN2ib...); utilities are not traced
-    if (std::strncmp(n, "_ZN2ib", 6) != 0 || std::strstr(n, "k_flush")) continue;
-    c.kernels.push_back((int64_t)k->start);
-    c.kernels.push_back((int64_t)k->end);
-  }
-  free(buffer);
-}
-
-}  // namespace
-
-struct ib_ctx {
-  int solver = 0, dtype = 0, esize = 8;
-  int64_t dims[3] = {1, 1, 1};
-  int ndims = 1;
-  double scalars[3] = {0, 0, 0};
-  std::vector<Slab> slabs;
-  void *field[6] = {};      // vector / fdtd device fields (single slab)
-  void *field2[6] = {};     // fused fdtd: the second buffer of the ping-pong field pairs
-  // fused fdtd: the padded lattice (two parities), fields at lat[p] + f*lat_fs elements, rows of
-  // lat_pitch elements (nz+1 rounded up to 16 bytes); field/field2 point into it
-  void *lat[2] = {nullptr, nullptr};
-  int64_t lat_pitch = 0, lat_fs = 0;
-  int64_t fshape[6][3] = {};
-  int fndim[6] = {};
-  int nfields = 0;
-  int cur = 0;              // hotspot ping-pong parity: buf[cur] holds the current temperature
-  int num_sms = 148;        // of slab 0's device
-  cudaEvent_t t0 = nullptr, t1 = nullptr;
-  cudaStream_t cap_stream = nullptr;  // used only for stream capture of single-slab graphs
-  // graph state
-  int64_t K = 0;
-  int gflags = 0, gmode = 0;
-  cudaGraph_t graph[2] = {nullptr, nullptr};
-  cudaGraphExec_t exec[2] = {nullptr, nullptr};  // indexed by start parity
-  cudaGraphConditionalHandle cond[2] = {};
-  int *d_counter = nullptr;  // WHILE-mode remaining-batch counter
-  void *flush = nullptr;
-  size_t flush_bytes = 0;
-  // multi-process slab (ib_create_dist)
-  int rank = 0, nranks = 1;
-  void *comm = nullptr;  // ncclComm_t (NCCL exchange)
-  // peer exchange (ib_ipc_attach): the stencil kernel stores its boundary planes straight into the
-  // neighbour ranks' halo planes through CUDA IPC mappings; cross-process ordering by device-side
-  // iteration counters (k_dist_wait / k_dist_signal, one pair per iteration inside the graph)
-  unsigned long long *sync = nullptr;        // [0] my completed iterations, [1] up's, [2] down's
-  void *peer_buf_up[2] = {nullptr, nullptr}, *peer_buf_dn[2] = {nullptr, nullptr};
-  unsigned long long *peer_sync_up = nullptr, *peer_sync_dn = nullptr;
-  int peer_rows_up = 0;  // the up neighbour's owned rows (locates its bottom halo plane)
-  int peer_rows_dn = 0;  // the down neighbour's (FDTD: its lattice field stride)
-  bool peer = false;
-  bool dist() const { return nranks > 1; }
-  int64_t lattice_pitch() const { return lat_pitch; }
-  // tracing (CUPTI activity records; host events on the CUPTI timebase)
-  bool tracing = false;
-  int64_t trace_cap = 0;
-  struct HostEv { int64_t t, kind, batch, kernel; };
-  std::vector<HostEv> host_ev;
-  void ev(int kind, int64_t batch = -1, int64_t kernel = -1);
-
-  cudaStream_t stream() const { return slabs[0].stream; }
-  bool ping_pong() const {
-    return solver == IB_SOLVER_HOTSPOT2D || solver == IB_SOLVER_HOTSPOT3D ||
-           solver == IB_SOLVER_FDTD_FUSED;
-  }
-  bool fdtd() const { return solver == IB_SOLVER_FDTD || solver == IB_SOLVER_FDTD_FUSED; }
-  bool hotspot() const { return solver == IB_SOLVER_HOTSPOT2D || solver == IB_SOLVER_HOTSPOT3D; }
-  void *fieldp(int f, int parity) const {  // device field f holding parity `parity`
-    return (solver == IB_SOLVER_FDTD_FUSED && parity) ? field2[f] : field[f];
-  }
-  int64_t plane() const {  // elements per axis-0 plane (hotspot)
-    return solver == IB_SOLVER_HOTSPOT3D ? dims[1] * dims[2] : dims[1];
-  }
-};
-
-void ib_ctx::ev(int kind, int64_t batch, int64_t kernel) {
-  if (!tracing) return;
-  uint64_t t = 0;
-  cupti().GetTimestamp(&t);
-  host_ev.push_back({(int64_t)t, kind, batch, kernel});
-}
-
-namespace {
-
-int64_t numel(const int64_t *s, int n) {
-  int64_t r = 1;
-  for (int i = 0; i < n; ++i) r *= s[i];
-  return r;
-}
-
-// ---- per-iteration launch lists ----------------------------------------------------------------
-int hotspot_rows_per_chunk(const ib_ctx *c, int rows) {
-  int64_t rpc = env_int("IB_HOTSPOT_RPC", 0);
-  if (rpc <= 0) {
-    const int64_t want_threads = 148LL * 2048 * 2;
-    int64_t chunks = (want_threads + c->plane() - 1) / c->plane();
-    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, rows));
-    rpc = (rows + chunks - 1) / chunks;
-    rpc = std::min<int64_t>(rpc, 64);
-  }
-  return (int)std::max<int64_t>(1, std::min<int64_t>(rpc, rows));
-}
-
-// Kernel variant for a hotspot grid. IB_HOTSPOT_KERNEL=scalar|vec|tma forces one (if legal).
-//   vec    one 16-byte group per thread, every load independent: best for L2-resident grids
-//   tma    cp.async.bulk plane-march pipeline: best once the state no longer fits in L2
-//   scalar marching fallback for shapes the vector paths cannot take (M or L not a multiple of V)
-enum class HotKernel { Scalar, Vec, Tma };
-
-template <typename T>
-int tma_groups(const ib_ctx *c) {  // G such that TM = G*V*256 holds whole y-rows; 0 = not possible
-  constexpr int V = 16 / sizeof(T);
-  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
-  const int64_t L = d3 ? c->dims[2] : 1;
-  for (int G : {2, 1, 4}) {
-    const int64_t TM = (int64_t)G * V * 256;
-    if (!d3 || (TM % L == 0 && L <= 1024)) return G;
-  }
-  return 0;
-}
-
-template <typename T>
-HotKernel hotspot_variant(const ib_ctx *c, int rows) {
-  constexpr int V = 16 / sizeof(T);
-  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
-  const int64_t M = c->plane();
-  const int64_t L = d3 ? c->dims[2] : 1;
-  const bool vec_ok = (M % V == 0) && (!d3 || L % V == 0) && rows <= 65535 &&
-                      (int64_t)(rows + 2) * M < (1LL << 31);  // 32-bit offsets
-  const bool tma_ok = vec_ok && tma_groups<T>(c) > 0 && rows >= 2;
-  const char *force = env_str("IB_HOTSPOT_KERNEL");
-  if (force) {
-    if (!std::strcmp(force, "tma") && tma_ok) return HotKernel::Tma;
-    if (!std::strcmp(force, "vec") && vec_ok) return HotKernel::Vec;
-    if (!std::strcmp(force, "scalar")) return HotKernel::Scalar;
-  }
-  const int64_t state_bytes = 3 * M * c->dims[0] * (int64_t)sizeof(T);
-  if (tma_ok && state_bytes >= (96LL << 20)) return HotKernel::Tma;
-  if (vec_ok) return HotKernel::Vec;
-  return HotKernel::Scalar;
-}
-
-template <typename T, bool D3>
-const void *tma_fn(int G) {
-  switch (G) {
-    case 1: return (const void *)ib::k_hotspot_tma<T, D3, 1>;
-    case 4: return (const void *)ib::k_hotspot_tma<T, D3, 4>;
-    default: return (const void *)ib::k_hotspot_tma<T, D3, 2>;
-  }
-}
-
-template <typename T, bool D3, int SH>
-const void *vec_fn_r(int R) {
-  return R >= 4 ? (const void *)ib::k_hotspot_vec<T, D3, 4, SH>
-                : R == 2 ? (const void *)ib::k_hotspot_vec<T, D3, 2, SH> : (const void *)ib::k_hotspot_vec<T, D3, 1, SH>;
-}
-template <typename T>
-const void *vec_fn(bool d3, int R, int sh) {
-  if (d3) return sh == 2 ? vec_fn_r<T, true, 2>(R) : sh == 1 ? vec_fn_r<T, true, 1>(R) : vec_fn_r<T, true, 0>(R);
-  return sh ? vec_fn_r<T, false, 1>(R) : vec_fn_r<T, false, 0>(R);
-}
-
-template <typename T>
-void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
-  constexpr int V = 16 / sizeof(T);
-  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
-  const int C = (int)c->dims[1];
-  const int L = d3 ? (int)c->dims[2] : 1;
-  const int64_t plane = c->plane();
-  const T k = (T)c->scalars[0];
-  const T loss = (T)(2.0 * (d3 ? 3 : 2));
-  const int P = (int)c->slabs.size();
-  const bool multi = P > 1 || c->dist();  // slab buffers carry halo planes
-  for (int g = 0; g < P; ++g) {
-    Slab &s = c->slabs[g];
-    const int rows = s.rows();
-    const int64_t off = multi ? plane : 0;  // first owned plane
-    const T *src = (const T *)s.buf[parity] + off;
-    T *dst = (T *)s.buf[parity ^ 1] + off;
-    T *up = nullptr, *dn = nullptr;
-    if (P > 1 && g > 0) {  // my first owned row -> upper neighbour's bottom halo
-      Slab &n = c->slabs[g - 1];
-      up = (T *)n.buf[parity ^ 1] + (int64_t)(n.rows() + 1) * plane;
-    }
-    if (P > 1 && g + 1 < P) {  // my last owned row -> lower neighbour's top halo
-      Slab &n = c->slabs[g + 1];
-      dn = (T *)n.buf[parity ^ 1];
-    }
-    if (c->dist() && c->peer) {  // the neighbour ranks' halo planes, through IPC mappings
-      if (s.has_top) up = (T *)c->peer_buf_up[parity ^ 1] + (int64_t)(c->peer_rows_up + 1) * plane;
-      if (s.has_bot) dn = (T *)c->peer_buf_dn[parity ^ 1];
-    }
-    const int top = (int)s.has_top, bot = (int)s.has_bot;
-    dim3 block(256);
-    switch (hotspot_variant<T>(c, rows)) {
-      case HotKernel::Vec: {
-        // rows per thread (R+2 row loads per R outputs): with the neighbour loads (no shuffles)
-        // R = 1 — the most threads, the shortest per-thread chain — unless the grid would exceed
-        // four waves (measured: Hotspot3D 512x512x8 R=1 4.41, R=2 4.57, R=4 4.67 us/iter;
-        // Hotspot2D 1024^2 R=1 2.56, R=2 3.12); with shuffles R = 2 (below). IB_HOTSPOT_VEC_ROWS
-        // overrides.
-        int64_t R = env_int("IB_HOTSPOT_VEC_ROWS", 0);
-        const int64_t threads_per_row = plane / V;
-        // CTA shape: bx threads along a plane row (up to 256), by row-blocks, bx*by = IB_HOTSPOT_BLOCK.
-        // 256 measured best in-graph (Hotspot3D 512^2x8: 4.45 / 4.79 / 6.20 us at 256 / 512 / 1024;
-        // Hotspot2D 2.60 / 2.65 / 2.68) although an EMPTY kernel's launch floor falls with fewer,
-        // bigger CTAs (tools/microbench_floor.cu): real CTAs retire at their slowest warp.
-        // With shuffles and R = 2 (below), 2-D measured best at 512 threads (256 x 2 row-blocks:
-        // 2.33 vs 2.43 us/iter at 256), 3-D at 256 (4.21; 512: 4.61).
-        int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? 256 : 512);
-        bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
-        const int64_t bx = std::min<int64_t>(std::min<int64_t>(256, bs), (threads_per_row + 31) / 32 * 32);
-        const int64_t by = std::max<int64_t>(1, bs / bx);
-        const int64_t xblocks = (threads_per_row + bx - 1) / bx;
-        if (R <= 0) {
-          const int64_t slots = 1536LL * c->num_sms;  // resident threads at <= 40 registers
-          R = 1;
-          while (R < 4 && xblocks * bx * ((rows + R - 1) / R) > 4 * slots) R *= 2;
-        }
-        R = R >= 4 ? 4 : (R >= 2 ? 2 : 1);
-        // warp shuffles for the in-row (2-D) / z (3-D) neighbours when every warp covers 32 groups
-        // of one row and whole y-rows: 1 = those, 2 = also the y rows. IB_HOTSPOT_SHUFFLE overrides.
-        const int64_t gl = d3 ? L / V : 1;
-        // Measured in-graph with PDL (us/iter, two runs): Hotspot3D 512^2x8 R=1 4.47, R=1+sh1 4.36,
-        // R=2+sh1 4.22-4.25, sh2 (y rows by 8 shuffles) 4.60-4.77; Hotspot2D 1024^2 R=1 2.61,
-        // R=1+sh1 2.49, R=2+sh1 2.45. So z / row shuffles, and 2 rows per thread with them.
-        int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", 1);
-        if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
-        if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
-        const void *fn = vec_fn<T>(d3, (int)R, (int)std::min<int64_t>(sh, 2));
-        dim3 grid((unsigned)xblocks, (unsigned)((rows + R * by - 1) / (R * by)));
-        out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)by), g, src, dst, (const T *)s.power,
-                                  rows, C, L, k, loss,
-                                  top, bot, up, dn));
-        break;
-      }
-      case HotKernel::Tma: {
-        const int G = tma_groups<T>(c);
-        const int TM = G * V * 256;
-        const int H = d3 ? L : V;
-        const int ns = (int)std::max<int64_t>(3, std::min<int64_t>(8, env_int("IB_TMA_STAGES", 4)));
-        const size_t smem = (size_t)ns * (TM + 2 * H + TM) * sizeof(T) + (size_t)ns * 8;
-        const void *fn = d3 ? tma_fn<T, true>(G) : tma_fn<T, false>(G);
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int64_t tiles = (plane + TM - 1) / TM;
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
-        const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
-        int64_t rpc = env_int("IB_HOTSPOT_RPC", 0);
-        if (rpc <= 0) rpc = std::max<int64_t>(16, std::min<int64_t>(128, (int64_t)rows * tiles / (12 * slots)));
-        rpc = std::min<int64_t>(rpc, rows);
-        dim3 grid((unsigned)tiles, (unsigned)((rows + rpc - 1) / rpc));
-        Launch Lz = make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, (int)rpc, ns,
-                                k, loss, top, bot, up, dn);
-        Lz.smem = smem;
-        out.push_back(Lz);
-        break;
-      }
-      default: {
-        const void *fn = d3 ? (const void *)ib::k_hotspot<T, true> : (const void *)ib::k_hotspot<T, false>;
-        const int rpc = hotspot_rows_per_chunk(c, rows);
-        dim3 grid((unsigned)((plane + 255) / 256), (unsigned)((rows + rpc - 1) / rpc));
-        out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, rpc, k,
-                                  loss, top, bot, up, dn));
-      }
-    }
-  }
-}
-
-// Fused leapfrog (k_fdtd_lf): TJ y-rows per tile, NS-stage bulk-copy ring. The largest TJ (and
-// then NS) whose ring lets two CTAs share an SM; the grid is one wave of resident CTAs and the
-// (tile, plane) units are split evenly over it. IB_FDTD_TJ / IB_FDTD_STAGES override.
-struct LfConfig {
-  int tj = 0, ns = 0;
-  size_t smem = 0;
-};
-inline size_t lf_smem(int tj, int ns, int64_t P, int es) {
-  return (size_t)ns * (size_t)(3 * (tj + 2) + 3 * (tj + 1)) * (size_t)P * es + (size_t)ns * 8;
-}
-inline int lf_threads(const ib_ctx *c, int tj) {  // one thread per (row, 16-byte group)
-  const int64_t groups = c->lat_pitch / (16 / c->esize);
-  return (int)(((tj + 1) * groups + 31) / 32 * 32);
-}
-inline LfConfig lf_config(const ib_ctx *c) {
-  // The kernel is bound by the bytes each SM keeps in flight, CTAs/SM x (NS-1) x stage bytes.
-  // Measured at 256^3 binary32 (us/iter): TJ=4/NS=6/1 per SM 130.7, TJ=4/NS=5 137.3,
-  // TJ=3/NS=4/2 per SM 138.5, TJ=3/NS=3/2 per SM 196, TJ=4/NS=3/2 per SM 171. So: 4-row tiles
-  // with the deepest ring one CTA per SM holds (<= 6 stages), then 2 per SM, then smaller tiles.
-  const int64_t P = c->lat_pitch;
-  const int es = c->esize;
-  const size_t cap = 227 * 1024, half = 113 * 1024;
-  LfConfig cfg;
-  const int64_t ftj = env_int("IB_FDTD_TJ", 0), fns = env_int("IB_FDTD_STAGES", 0);
-  const struct { int tj; bool two; } order[] = {{4, false}, {3, true}, {4, true}, {2, true},
-                                                 {3, false}, {2, false}, {1, true}, {1, false}};
-  for (auto o : order) {
-    if (ftj > 0 && o.tj != ftj) continue;
-    if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
-    for (int ns = 3; ns <= 8; ++ns) {
-      if (fns > 0 && ns != fns) continue;
-      const size_t sm = lf_smem(o.tj, ns, P, es);
-      if (sm <= (o.two ? half : cap) && (fns > 0 || ns <= 6)) cfg = {o.tj, ns, sm};
-    }
-    if (cfg.tj && (cfg.ns >= 4 || fns > 0 || ftj > 0)) break;
-    if (cfg.tj && o.tj == 1) break;
-    if (cfg.tj && cfg.ns < 4) cfg = LfConfig{};  // too shallow: try the next shape
-  }
-  if (!cfg.tj) {  // nothing deep enough: take any shape that fits
-    for (auto o : order) {
-      if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
-      const size_t sm = lf_smem(o.tj, 3, P, es);
-      if (sm <= cap) { cfg = {o.tj, 3, sm}; break; }
-    }
-  }
-  return cfg;
-}
-
-template <typename T, bool U, int M>
-const void *lf_fn_m(int tj) {
-  switch (tj) {
-    case 1: return (const void *)ib::k_fdtd_lf<T, U, 1, M>;
-    case 2: return (const void *)ib::k_fdtd_lf<T, U, 2, M>;
-    case 3: return (const void *)ib::k_fdtd_lf<T, U, 3, M>;
-    default: return (const void *)ib::k_fdtd_lf<T, U, 4, M>;
-  }
-}
-template <typename T>
-const void *lf_fn(bool unit, int tj, int mode) {
-  if (unit) return mode == ib::kLfH ? lf_fn_m<T, true, ib::kLfH>(tj)
-                   : mode == ib::kLfE ? lf_fn_m<T, true, ib::kLfE>(tj) : lf_fn_m<T, true, ib::kLfFused>(tj);
-  return mode == ib::kLfH ? lf_fn_m<T, false, ib::kLfH>(tj)
-         : mode == ib::kLfE ? lf_fn_m<T, false, ib::kLfE>(tj) : lf_fn_m<T, false, ib::kLfFused>(tj);
-}
-
-// One k_fdtd_lf launch of `mode` from lattice buffer `from` to `to` (equal for the in-place
-// half-steps).
-template <typename T>
-Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int64_t fs, void *halo_h = nullptr,
-                 int64_t fs_h = 0, void *halo_e = nullptr, int64_t fs_e = 0, int slab = 0) {
-  const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
-  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
-  const bool unit = c->scalars[0] == 1.0;
-  const LfConfig cfg = lf_config(c);
-  const void *fn = lf_fn<T>(unit, cfg.tj, mode);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
-  const int threads = lf_threads(c, cfg.tj);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, cfg.smem);
-  // Lockstep (tile, x-chunk) grid: as many x-chunks as the resident slots hold whole columns of
-  // TJ-row tiles (256^3, TJ=4, 148 slots: 65 tiles x 2 chunks). Filling the spare slots with
-  // shorter tiles (74 tiles of 3-4 rows x 2) measured slower (137 vs 131 us): more halo rows.
-  // IB_FDTD_TILES (uneven rows, h <= TJ), IB_FDTD_CHUNKS, IB_FDTD_CTAS (even split) override.
-  const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
-  const int64_t min_tiles = (ny + 1 + cfg.tj - 1) / cfg.tj;
-  int64_t tiles = min_tiles;
-  if (env_int("IB_FDTD_TILES", 0) >= min_tiles) tiles = std::min<int64_t>(ny + 1, env_int("IB_FDTD_TILES", 0));
-  int64_t chunks = env_int("IB_FDTD_CHUNKS", 0);
-  if (chunks <= 0) chunks = std::max<int64_t>(1, slots / tiles);
-  chunks = std::min<int64_t>(chunks, npl);  // every chunk non-empty
-  int64_t ctas = env_int("IB_FDTD_CTAS", 0);
-  if (ctas <= 0) {
-    ctas = tiles * chunks;  // one CTA per (tile, chunk): the kernel maps blockIdx.x to both
-  } else {
-    chunks = 0;  // even split of the tile-major unit list over `ctas` CTAs
-    ctas = std::max<int64_t>(1, std::min(ctas, tiles * npl));
-  }
-  Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), slab, (const T *)from, (T *)to, nx,
-                         ny, nz, (int)c->lat_pitch, fs, x0, npl, (int)tiles, (int)chunks, cfg.ns, ch, ce, d,
-                         (T *)halo_h, fs_h, (T *)halo_e, fs_e);
-  L.smem = cfg.smem;
-  L.step = mode == ib::kLfE ? 1 : 0;
-  return L;
-}
-
-// FDTD, the reference's two half-steps (H then E, in place on the lattice): k_fdtd_lf in its H
-// and E modes, or the lean one-thread-per-point kernels when the z rows are too long for the
-// staged kernel's CTA (or IB_FDTD_KERNEL=lean).
-template <typename T>
-void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
-  const char *force = env_str("IB_FDTD_KERNEL");
-  const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0;
-  const int nx = (int)c->dims[0];
-  const int P = (int)c->slabs.size();
-  if (c->dist()) {  // one rank's slab; the neighbours' halo planes through IPC mappings
-    const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lattice_pitch();
-    Slab &s = c->slabs[0];
-    T *base = (T *)s.buf[0] + (int64_t)(1 - s.row_lo) * plane;
-    void *hh = nullptr, *he = nullptr;
-    int64_t fh = 0, fe = 0;
-    if (c->peer && s.has_bot) {
-      hh = c->peer_buf_dn[0];  // the down rank's top halo plane (its local 0)
-      fh = (int64_t)(c->peer_rows_dn + 2) * plane;
-    }
-    if (c->peer && s.has_top) {
-      he = (T *)c->peer_buf_up[0] + (int64_t)(c->peer_rows_up + 1) * plane;  // the up rank's bottom halo
-      fe = (int64_t)(c->peer_rows_up + 2) * plane;
-    }
-    out.push_back(lf_launch<T>(c, ib::kLfH, base, base, s.row_lo, s.rows(), s.fs, hh, fh, nullptr, 0, 0));
-    out.push_back(lf_launch<T>(c, ib::kLfE, base, base, s.row_lo, s.rows(), s.fs, nullptr, 0, he, fe, 0));
-    return;
-  }
-  if (P > 1) {  // axis-0 slabs: every H launch, then every E launch, halo planes pushed in-kernel
-    const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lat_pitch;
-    for (int step = 0; step < 2; ++step)
-      for (int g = 0; g < P; ++g) {
-        Slab &s = c->slabs[g];
-        T *base = (T *)s.buf[0] + (int64_t)(1 - s.row_lo) * plane;  // global plane index -> buffer
-        void *hh = nullptr, *he = nullptr;
-        int64_t fh = 0, fe = 0;
-        if (step == 0 && g + 1 < P) {
-          hh = c->slabs[g + 1].buf[0];  // its top halo plane (local 0)
-          fh = c->slabs[g + 1].fs;
-        }
-        if (step == 1 && g > 0) {
-          Slab &n = c->slabs[g - 1];
-          he = (T *)n.buf[0] + (int64_t)(n.rows() + 1) * plane;  // its bottom halo plane
-          fe = n.fs;
-        }
-        out.push_back(lf_launch<T>(c, step == 0 ? ib::kLfH : ib::kLfE, base, base, s.row_lo, s.rows(), s.fs,
-                                   hh, fh, he, fe, g));
-      }
-    return;
-  }
-  if (!lean) {
-    out.push_back(lf_launch<T>(c, ib::kLfH, c->lat[0], c->lat[0], 0, nx + 1, c->lat_fs));
-    out.push_back(lf_launch<T>(c, ib::kLfE, c->lat[0], c->lat[0], 0, nx + 1, c->lat_fs));
-    return;
-  }
-  const int ny = (int)c->dims[1], nz = (int)c->dims[2];
-  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
-  const bool unit = c->scalars[0] == 1.0;
-  dim3 b2(32, 8);
-  dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)(nx + 1));
-  const void *fh = unit ? (const void *)ib::k_fdtd_h2<T, true> : (const void *)ib::k_fdtd_h2<T, false>;
-  const void *fe = unit ? (const void *)ib::k_fdtd_e2<T, true> : (const void *)ib::k_fdtd_e2<T, false>;
-  T *f = (T *)c->lat[0];
-  out.push_back(make_launch(fh, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ch, d));
-  out.push_back(make_launch(fe, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ce, d));
-  out.back().step = 1;
-}
-
-// FDTD fused: one k_fdtd_lf launch per iteration, parity -> parity ^ 1.
-template <typename T>
-void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
-  out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1], 0, (int)c->dims[0] + 1,
-                             c->lat_fs));
-}
-
-void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
-  out.clear();
-  switch (c->solver) {
-    case IB_SOLVER_VECTOR: {
-      const int64_t n = c->dims[0];
-      const double cc = c->scalars[0];
-      // 128-thread CTAs measured best (1.21 / 1.23 / 1.24 / 1.40 us per iteration in a PDL graph at
-      // 128 / 256 / 512 / 1024); IB_VECTOR_BLOCK overrides
-      int64_t bs = env_int("IB_VECTOR_BLOCK", 128);
-      bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
-      if (c->dtype == IB_F32) {
-        const int64_t threads = (n >> 2) + (n & 3);
-        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
-        out.push_back(make_launch((const void *)ib::k_vector_f32, grid, block, 0,
-                                  (float *)c->field[0], n, cc));
-      } else {
-        const int64_t threads = (n >> 1) + (n & 1);
-        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
-        out.push_back(make_launch((const void *)ib::k_vector_f64, grid, block, 0,
-                                  (double *)c->field[0], n, cc));
-      }
-      break;
-    }
-    case IB_SOLVER_HOTSPOT2D:
-    case IB_SOLVER_HOTSPOT3D:
-      if (c->dtype == IB_F32)
-        hotspot_launches<float>(c, parity, out);
-      else
-        hotspot_launches<double>(c, parity, out);
-      break;
-    case IB_SOLVER_FDTD:
-      if (c->dtype == IB_F32)
-        fdtd_launches<float>(c, out);
-      else
-        fdtd_launches<double>(c, out);
-      break;
-    case IB_SOLVER_FDTD_FUSED:
-      if (c->dtype == IB_F32)
-        fdtd_fused_launches<float>(c, parity, out);
-      else
-        fdtd_fused_launches<double>(c, parity, out);
-      break;
-  }
-}
-
-int launch_one(Launch &L, cudaStream_t s, bool pdl) {
-  if (!pdl) {
-    IB_CUDA(cudaLaunchKernel(L.func, L.grid, L.block, L.args(), L.smem, s));
-    return IB_OK;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = L.grid;
-  cfg.blockDim = L.block;
-  cfg.dynamicSmemBytes = L.smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  IB_CUDA(cudaLaunchKernelExC(&cfg, L.func, L.args()));
-  return IB_OK;
-}
-
-// Halo exchange of a distributed slab after an iteration that wrote buf[parity]:
-// send my first owned plane to rank-1 and receive its last into my top halo; the mirror with
-// rank+1. One NCCL group, on the launch stream (captured into graphs like the kernels).
-int nccl_exchange(ib_ctx *c, int parity, cudaStream_t st) {
-  Nccl &n = nccl();
-  Slab &s = c->slabs[0];
-  const size_t pb = (size_t)(c->plane() * c->esize);
-  char *b = (char *)s.buf[parity];
-  auto chk = [&](int r, const char *what) {
-    if (r != 0) return fail(IB_ECUDA, std::string(what) + ": " + n.GetErrorString(r));
-    return IB_OK;
-  };
-  IB_TRY(chk(n.GroupStart(), "ncclGroupStart"));
-  if (s.has_top) {
-    IB_TRY(chk(n.Send(b + pb, pb, kNcclInt8, c->rank - 1, c->comm, st), "ncclSend(up)"));
-    IB_TRY(chk(n.Recv(b, pb, kNcclInt8, c->rank - 1, c->comm, st), "ncclRecv(up)"));
-  }
-  if (s.has_bot) {
-    IB_TRY(chk(n.Send(b + (size_t)s.rows() * pb, pb, kNcclInt8, c->rank + 1, c->comm, st), "ncclSend(down)"));
-    IB_TRY(chk(n.Recv(b + (size_t)(s.rows() + 1) * pb, pb, kNcclInt8, c->rank + 1, c->comm, st), "ncclRecv(down)"));
-  }
-  IB_TRY(chk(n.GroupEnd(), "ncclGroupEnd"));
-  return IB_OK;
-}
-
-int launch_dist_wait(ib_ctx *c, cudaStream_t st) {
-  const int top = c->slabs[0].has_top, bot = c->slabs[0].has_bot;
-  Launch L = make_launch((const void *)ib::k_dist_wait, dim3(1), dim3(1), 0, (const unsigned long long *)c->sync,
-                         top, bot, (long long)env_int("IB_DIST_TIMEOUT_MS", 20000));
-  return launch_one(L, st, false);
-}
-int launch_dist_signal(ib_ctx *c, cudaStream_t st) {
-  Launch L = make_launch((const void *)ib::k_dist_signal, dim3(1), dim3(1), 0, c->sync, c->peer_sync_up,
-                         c->peer_sync_dn);
-  return launch_one(L, st, false);
-}
-
-// Enqueue `iters` iterations starting at `parity` onto the slab streams (also used under stream
-// capture). Multi-slab: kernel(g,t) waits for kernel(g+-1,t-1) — RAW on the halo it reads and
-// WAR on the halo it writes — through double-buffered events.
-int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStream_t single_stream,
-                       int64_t *kernels, int64_t *launches) {
-  std::vector<Launch> its[2];
-  iteration_launches(c, 0, its[0]);
-  if (c->ping_pong()) iteration_launches(c, 1, its[1]);
-  const int P = (int)c->slabs.size();
-  int steps = 1;  // half-steps per iteration (launches are listed step-major)
-  for (const Launch &L : its[0]) steps = std::max(steps, L.step + 1);
-  int par = parity;
-  int64_t nk = 0;
-  for (int64_t t = 0; t < iters; ++t) {
-    std::vector<Launch> &v = c->ping_pong() ? its[par] : its[0];
-    for (size_t q = 0; q < v.size(); ++q) {
-      Launch &L = v[q];
-      Slab &s = c->slabs[L.slab];
-      cudaStream_t st = (P == 1 && single_stream) ? single_stream : s.stream;
-      // phase = global half-step index; a slab's launch of phase f waits for its neighbours'
-      // launches of phase f-1 (RAW on the halo it reads, WAR on the halo it writes)
-      const int64_t f = t * steps + L.step;
-      if (P > 1) {
-        IB_CUDA(cudaSetDevice(s.device));
-        if (f > 0) {
-          if (L.slab > 0) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab - 1].ev[(f - 1) & 1], 0));
-          if (L.slab + 1 < P) IB_CUDA(cudaStreamWaitEvent(st, c->slabs[L.slab + 1].ev[(f - 1) & 1], 0));
-        }
-      }
-      // PDL only chains kernels on the same stream; the very first launch has no predecessor.
-      // Peer-exchange contexts never use it: the wait / signal kernels must not overlap the stencil.
-      const bool use_pdl = pdl && P == 1 && (t > 0 || q > 0) && !c->peer;
-      if (c->peer) IB_TRY(launch_dist_wait(c, st));  // neighbours done with the previous phase
-      c->ev(single_stream ? IB_EV_NODE_ADDED : IB_EV_BASELINE_KERNEL_LAUNCHED, single_stream ? -1 : t,
-            single_stream ? nk : (int64_t)q);
-      IB_TRY(launch_one(L, st, use_pdl));
-      if (P > 1) IB_CUDA(cudaEventRecord(s.ev[f & 1], st));
-      if (c->peer) IB_TRY(launch_dist_signal(c, st));  // its halo planes went out with its stores
-      ++nk;
-    }
-    if (c->dist()) {  // boundary planes of this iteration's output <-> neighbouring ranks
-      cudaStream_t st = single_stream ? single_stream : c->slabs[0].stream;
-      if (!c->peer) IB_TRY(nccl_exchange(c, par ^ 1, st));
-    }
-    if (c->ping_pong()) par ^= 1;
-  }
-  if (P > 1) IB_CUDA(cudaSetDevice(c->slabs[0].device));
-  if (kernels) *kernels += nk;
-  if (launches) *launches += nk;
-  return IB_OK;
-}
-
-// Join all slab streams into slab 0's stream (or fork from it).
-int join_into(ib_ctx *c, cudaStream_t root, bool fork) {
-  if (c->slabs.size() == 1) return IB_OK;
-  if (fork) {
-    IB_CUDA(cudaSetDevice(c->slabs[0].device));
-    IB_CUDA(cudaEventRecord(c->slabs[0].join, root));
-  }
-  for (size_t g = 1; g < c->slabs.size(); ++g) {
-    Slab &s = c->slabs[g];
-    IB_CUDA(cudaSetDevice(s.device));
-    if (fork) {
-      IB_CUDA(cudaStreamWaitEvent(s.stream, c->slabs[0].join, 0));
-    } else {
-      IB_CUDA(cudaEventRecord(s.join, s.stream));
-      IB_CUDA(cudaSetDevice(c->slabs[0].device));
-      IB_CUDA(cudaStreamWaitEvent(root, s.join, 0));
-    }
-  }
-  IB_CUDA(cudaSetDevice(c->slabs[0].device));
-  return IB_OK;
-}
-
-void free_graphs(ib_ctx *c) {
-  for (int p = 0; p < 2; ++p) {
-    if (c->exec[p]) cudaGraphExecDestroy(c->exec[p]);
-    if (c->graph[p]) cudaGraphDestroy(c->graph[p]);
-    c->exec[p] = nullptr;
-    c->graph[p] = nullptr;
-  }
-  c->K = 0;
-}
-
-// Listing 3: cudaGraphCreate + a linear chain of cudaGraphAddKernelNode.
-// With IB_FLAG_PDL the chain edges are programmatic (kernel t+1 may be resident before t ends).
-int build_manual_chain(ib_ctx *c, cudaGraph_t graph, int64_t K, int parity, bool pdl,
-                       cudaGraphNode_t *first, cudaGraphNode_t *last, int64_t *nodes) {
-  std::vector<Launch> its[2];
-  iteration_launches(c, 0, its[0]);
-  if (c->ping_pong()) iteration_launches(c, 1, its[1]);
-  cudaGraphNode_t prev = nullptr;
-  int par = parity;
-  for (int64_t t = 0; t < K; ++t) {
-    std::vector<Launch> &v = c->ping_pong() ? its[par] : its[0];
-    for (Launch &L : v) {
-      cudaKernelNodeParams np = {};
-      np.func = const_cast<void *>(L.func);
-      np.gridDim = L.grid;
-      np.blockDim = L.block;
-      np.sharedMemBytes = (unsigned)L.smem;
-      np.kernelParams = L.args();
-      np.extra = nullptr;
-      cudaGraphNode_t node;
-      if (!prev) {
-        IB_CUDA(cudaGraphAddKernelNode(&node, graph, nullptr, 0, &np));
-        if (first) *first = node;
-      } else if (!pdl) {
-        IB_CUDA(cudaGraphAddKernelNode(&node, graph, &prev, 1, &np));
-      } else {
-        IB_CUDA(cudaGraphAddKernelNode(&node, graph, nullptr, 0, &np));
-        cudaGraphEdgeData ed = {};
-        ed.from_port = cudaGraphKernelNodePortProgrammatic;
-        ed.type = cudaGraphDependencyTypeProgrammatic;
-        IB_CUDA(cudaGraphAddDependencies_v2(graph, &prev, &node, &ed, 1));
-      }
-      prev = node;
-      c->ev(IB_EV_NODE_ADDED, -1, *nodes);
-      ++*nodes;
-    }
-    if (c->ping_pong()) par ^= 1;
-  }
-  if (last) *last = prev;
-  return IB_OK;
-}
-
-}  // namespace
-
-// Device-side tail of a WHILE body: decrement the remaining-batch counter and keep looping while
-// batches remain (cudaGraphSetConditional, CUDA 12.4+ conditional nodes).
-__global__ void k_while_tick(int *counter, cudaGraphConditionalHandle h) {
-  int left = *counter - 1;
-  *counter = left;
-  cudaGraphSetConditional(h, left > 0 ? 1u : 0u);
-}
-
-namespace {
-
-// Build one executable graph starting at `parity`.
-int build_one(ib_ctx *c, int parity, ib_times *tm) {
-  const bool pdl = (c->gflags & IB_FLAG_PDL) != 0;
-  const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
-  const int P = (int)c->slabs.size();
-  int64_t nodes = 0;
-  NvtxRange range("ib graph build (create + instantiate + upload)");
-  c->ev(IB_EV_BUILD_STARTED);
-  auto a = clk::now();
-  cudaGraph_t g = nullptr;
-  if (c->gmode == IB_BUILD_MANUAL && P == 1 && !c->dist()) {
-    IB_CUDA(cudaGraphCreate(&g, 0));
-    cudaGraph_t body = g;
-    if (wh) {
-      // graph = [WHILE node { K-chain ; tick }]; the counter is set before each launch.
-      IB_CUDA(cudaGraphConditionalHandleCreate(&c->cond[parity], g, 1, cudaGraphCondAssignDefault));
-      cudaGraphNodeParams cp = {};
-      cp.type = cudaGraphNodeTypeConditional;
-      cp.conditional.handle = c->cond[parity];
-      cp.conditional.type = cudaGraphCondTypeWhile;
-      cp.conditional.size = 1;
-      cudaGraphNode_t wnode;
-      IB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &cp));
-      body = cp.conditional.phGraph_out[0];
-      ++nodes;
-    }
-    cudaGraphNode_t last = nullptr;
-    IB_TRY(build_manual_chain(c, body, c->K, parity, pdl, nullptr, &last, &nodes));
-    if (wh) {
-      cudaKernelNodeParams np = {};
-      int *cnt = c->d_counter;
-      cudaGraphConditionalHandle h = c->cond[parity];
-      void *args[2] = {&cnt, &h};
-      np.func = (void *)k_while_tick;
-      np.gridDim = dim3(1);
-      np.blockDim = dim3(1);
-      np.kernelParams = args;
-      cudaGraphNode_t tick;
-      IB_CUDA(cudaGraphAddKernelNode(&tick, body, &last, 1, &np));
-      ++nodes;
-    }
-  } else {
-    if (wh) return fail(IB_EINVAL, "IB_FLAG_WHILE requires IB_BUILD_MANUAL on a single slab");
-    // Stream capture of exactly the stream-mode launch sequence.
-    cudaStream_t root = (P == 1) ? c->cap_stream : c->slabs[0].stream;
-    IB_CUDA(cudaSetDevice(c->slabs[0].device));
-    IB_CUDA(cudaStreamBeginCapture(root, cudaStreamCaptureModeThreadLocal));
-    int rc = join_into(c, root, true);
-    int64_t kk = 0, ll = 0;
-    if (rc == IB_OK) rc = enqueue_iterations(c, c->K, parity, pdl, P == 1 ? root : nullptr, &kk, &ll);
-    if (rc == IB_OK) rc = join_into(c, root, false);
-    cudaError_t e = cudaStreamEndCapture(root, &g);
-    if (rc != IB_OK) {
-      if (g) cudaGraphDestroy(g);
-      return rc;
-    }
-    IB_CUDA(e);
-    size_t n = 0;
-    IB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
-    nodes += (int64_t)n;
-  }
-  auto b = clk::now();
-  unsigned long long iflags = 0;
-  if (c->gflags & IB_FLAG_DEVICE_LAUNCH) iflags |= cudaGraphInstantiateFlagDeviceLaunch;
-  cudaGraphExec_t ex = nullptr;
-  cudaError_t ie = cudaGraphInstantiateWithFlags(&ex, g, iflags);
-  if (ie != cudaSuccess) {
-    cudaGraphDestroy(g);
-    return fail(IB_ECUDA, std::string("cudaGraphInstantiateWithFlags: ") + cudaGetErrorString(ie));
-  }
-  auto d = clk::now();
-  c->ev(IB_EV_GRAPH_INSTANTIATED);
-  if (!(c->gflags & IB_FLAG_NO_UPLOAD)) {
-    IB_CUDA(cudaGraphUpload(ex, c->stream()));
-    IB_CUDA(cudaStreamSynchronize(c->stream()));
-  }
-  auto e2 = clk::now();
-  c->ev(IB_EV_GRAPH_UPLOADED);
-  c->graph[parity] = g;
-  c->exec[parity] = ex;
-  if (tm) {
-    tm->create_s += secs(a, b);
-    tm->instantiate_s += secs(b, d);
-    tm->upload_s += secs(d, e2);
-    tm->build_s += secs(a, e2);
-    tm->nodes += nodes;
-  }
-  return IB_OK;
-}
-
-int check_ctx(const ib_ctx *c) {
-  if (!c) return fail(IB_EINVAL, "null context");
-  return IB_OK;
-}
-
-}  // namespace
+#include "runtime_core.cuh"
+#include "runtime_ctx.cuh"
+#include "runtime_launches.cuh"
+#include "runtime_graphs.cuh"
 
 // ================================================================================================
 // C ABI

@@ -1,0 +1,416 @@
+// runtime_launches.cuh — per-iteration kernel launch lists: vector, hotspot variants, FDTD (k_fdtd_lf modes, lean fallback, slabs, ranks).
+// Part of runtime.cu (one translation unit; included in order, not compiled alone).
+#pragma once
+
+namespace {
+
+int64_t numel(const int64_t *s, int n) {
+  int64_t r = 1;
+  for (int i = 0; i < n; ++i) r *= s[i];
+  return r;
+}
+
+// ---- per-iteration launch lists ----------------------------------------------------------------
+int hotspot_rows_per_chunk(const ib_ctx *c, int rows) {
+  int64_t rpc = env_int("IB_HOTSPOT_RPC", 0);
+  if (rpc <= 0) {
+    const int64_t want_threads = 148LL * 2048 * 2;
+    int64_t chunks = (want_threads + c->plane() - 1) / c->plane();
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, rows));
+    rpc = (rows + chunks - 1) / chunks;
+    rpc = std::min<int64_t>(rpc, 64);
+  }
+  return (int)std::max<int64_t>(1, std::min<int64_t>(rpc, rows));
+}
+
+// Kernel variant for a hotspot grid. IB_HOTSPOT_KERNEL=scalar|vec|tma forces one (if legal).
+//   vec    one 16-byte group per thread, every load independent: best for L2-resident grids
+//   tma    cp.async.bulk plane-march pipeline: best once the state no longer fits in L2
+//   scalar marching fallback for shapes the vector paths cannot take (M or L not a multiple of V)
+enum class HotKernel { Scalar, Vec, Tma };
+
+template <typename T>
+int tma_groups(const ib_ctx *c) {  // G such that TM = G*V*256 holds whole y-rows; 0 = not possible
+  constexpr int V = 16 / sizeof(T);
+  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
+  const int64_t L = d3 ? c->dims[2] : 1;
+  for (int G : {2, 1, 4}) {
+    const int64_t TM = (int64_t)G * V * 256;
+    if (!d3 || (TM % L == 0 && L <= 1024)) return G;
+  }
+  return 0;
+}
+
+template <typename T>
+HotKernel hotspot_variant(const ib_ctx *c, int rows) {
+  constexpr int V = 16 / sizeof(T);
+  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
+  const int64_t M = c->plane();
+  const int64_t L = d3 ? c->dims[2] : 1;
+  const bool vec_ok = (M % V == 0) && (!d3 || L % V == 0) && rows <= 65535 &&
+                      (int64_t)(rows + 2) * M < (1LL << 31);  // 32-bit offsets
+  const bool tma_ok = vec_ok && tma_groups<T>(c) > 0 && rows >= 2;
+  const char *force = env_str("IB_HOTSPOT_KERNEL");
+  if (force) {
+    if (!std::strcmp(force, "tma") && tma_ok) return HotKernel::Tma;
+    if (!std::strcmp(force, "vec") && vec_ok) return HotKernel::Vec;
+    if (!std::strcmp(force, "scalar")) return HotKernel::Scalar;
+  }
+  const int64_t state_bytes = 3 * M * c->dims[0] * (int64_t)sizeof(T);
+  if (tma_ok && state_bytes >= (96LL << 20)) return HotKernel::Tma;
+  if (vec_ok) return HotKernel::Vec;
+  return HotKernel::Scalar;
+}
+
+template <typename T, bool D3>
+const void *tma_fn(int G) {
+  switch (G) {
+    case 1: return (const void *)ib::k_hotspot_tma<T, D3, 1>;
+    case 4: return (const void *)ib::k_hotspot_tma<T, D3, 4>;
+    default: return (const void *)ib::k_hotspot_tma<T, D3, 2>;
+  }
+}
+
+template <typename T, bool D3, int SH>
+const void *vec_fn_r(int R) {
+  return R >= 4 ? (const void *)ib::k_hotspot_vec<T, D3, 4, SH>
+                : R == 2 ? (const void *)ib::k_hotspot_vec<T, D3, 2, SH> : (const void *)ib::k_hotspot_vec<T, D3, 1, SH>;
+}
+template <typename T>
+const void *vec_fn(bool d3, int R, int sh) {
+  if (d3) return sh == 2 ? vec_fn_r<T, true, 2>(R) : sh == 1 ? vec_fn_r<T, true, 1>(R) : vec_fn_r<T, true, 0>(R);
+  return sh ? vec_fn_r<T, false, 1>(R) : vec_fn_r<T, false, 0>(R);
+}
+
+template <typename T>
+void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  constexpr int V = 16 / sizeof(T);
+  const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
+  const int C = (int)c->dims[1];
+  const int L = d3 ? (int)c->dims[2] : 1;
+  const int64_t plane = c->plane();
+  const T k = (T)c->scalars[0];
+  const T loss = (T)(2.0 * (d3 ? 3 : 2));
+  const int P = (int)c->slabs.size();
+  const bool multi = P > 1 || c->dist();  // slab buffers carry halo planes
+  for (int g = 0; g < P; ++g) {
+    Slab &s = c->slabs[g];
+    const int rows = s.rows();
+    const int64_t off = multi ? plane : 0;  // first owned plane
+    const T *src = (const T *)s.buf[parity] + off;
+    T *dst = (T *)s.buf[parity ^ 1] + off;
+    T *up = nullptr, *dn = nullptr;
+    if (P > 1 && g > 0) {  // my first owned row -> upper neighbour's bottom halo
+      Slab &n = c->slabs[g - 1];
+      up = (T *)n.buf[parity ^ 1] + (int64_t)(n.rows() + 1) * plane;
+    }
+    if (P > 1 && g + 1 < P) {  // my last owned row -> lower neighbour's top halo
+      Slab &n = c->slabs[g + 1];
+      dn = (T *)n.buf[parity ^ 1];
+    }
+    if (c->dist() && c->peer) {  // the neighbour ranks' halo planes, through IPC mappings
+      if (s.has_top) up = (T *)c->peer_buf_up[parity ^ 1] + (int64_t)(c->peer_rows_up + 1) * plane;
+      if (s.has_bot) dn = (T *)c->peer_buf_dn[parity ^ 1];
+    }
+    const int top = (int)s.has_top, bot = (int)s.has_bot;
+    dim3 block(256);
+    switch (hotspot_variant<T>(c, rows)) {
+      case HotKernel::Vec: {
+        // rows per thread (R+2 row loads per R outputs): with the neighbour loads (no shuffles)
+        // R = 1 — the most threads, the shortest per-thread chain — unless the grid would exceed
+        // four waves (measured: Hotspot3D 512x512x8 R=1 4.41, R=2 4.57, R=4 4.67 us/iter;
+        // Hotspot2D 1024^2 R=1 2.56, R=2 3.12); with shuffles R = 2 (below). IB_HOTSPOT_VEC_ROWS
+        // overrides.
+        int64_t R = env_int("IB_HOTSPOT_VEC_ROWS", 0);
+        const int64_t threads_per_row = plane / V;
+        // CTA shape: bx threads along a plane row (up to 256), by row-blocks, bx*by = IB_HOTSPOT_BLOCK.
+        // 256 measured best in-graph (Hotspot3D 512^2x8: 4.45 / 4.79 / 6.20 us at 256 / 512 / 1024;
+        // Hotspot2D 2.60 / 2.65 / 2.68) although an EMPTY kernel's launch floor falls with fewer,
+        // bigger CTAs (tools/microbench_floor.cu): real CTAs retire at their slowest warp.
+        // With shuffles and R = 2 (below), 2-D measured best at 512 threads (256 x 2 row-blocks:
+        // 2.33 vs 2.43 us/iter at 256), 3-D at 256 (4.21; 512: 4.61).
+        int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? 256 : 512);
+        bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
+        const int64_t bx = std::min<int64_t>(std::min<int64_t>(256, bs), (threads_per_row + 31) / 32 * 32);
+        const int64_t by = std::max<int64_t>(1, bs / bx);
+        const int64_t xblocks = (threads_per_row + bx - 1) / bx;
+        if (R <= 0) {
+          const int64_t slots = 1536LL * c->num_sms;  // resident threads at <= 40 registers
+          R = 1;
+          while (R < 4 && xblocks * bx * ((rows + R - 1) / R) > 4 * slots) R *= 2;
+        }
+        R = R >= 4 ? 4 : (R >= 2 ? 2 : 1);
+        // warp shuffles for the in-row (2-D) / z (3-D) neighbours when every warp covers 32 groups
+        // of one row and whole y-rows: 1 = those, 2 = also the y rows. IB_HOTSPOT_SHUFFLE overrides.
+        const int64_t gl = d3 ? L / V : 1;
+        // Measured in-graph with PDL (us/iter, two runs): Hotspot3D 512^2x8 R=1 4.47, R=1+sh1 4.36,
+        // R=2+sh1 4.22-4.25, sh2 (y rows by 8 shuffles) 4.60-4.77; Hotspot2D 1024^2 R=1 2.61,
+        // R=1+sh1 2.49, R=2+sh1 2.45. So z / row shuffles, and 2 rows per thread with them.
+        int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", 1);
+        if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
+        if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
+        const void *fn = vec_fn<T>(d3, (int)R, (int)std::min<int64_t>(sh, 2));
+        dim3 grid((unsigned)xblocks, (unsigned)((rows + R * by - 1) / (R * by)));
+        out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)by), g, src, dst, (const T *)s.power,
+                                  rows, C, L, k, loss,
+                                  top, bot, up, dn));
+        break;
+      }
+      case HotKernel::Tma: {
+        const int G = tma_groups<T>(c);
+        const int TM = G * V * 256;
+        const int H = d3 ? L : V;
+        const int ns = (int)std::max<int64_t>(3, std::min<int64_t>(8, env_int("IB_TMA_STAGES", 4)));
+        const size_t smem = (size_t)ns * (TM + 2 * H + TM) * sizeof(T) + (size_t)ns * 8;
+        const void *fn = d3 ? tma_fn<T, true>(G) : tma_fn<T, false>(G);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t tiles = (plane + TM - 1) / TM;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+        const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
+        int64_t rpc = env_int("IB_HOTSPOT_RPC", 0);
+        if (rpc <= 0) rpc = std::max<int64_t>(16, std::min<int64_t>(128, (int64_t)rows * tiles / (12 * slots)));
+        rpc = std::min<int64_t>(rpc, rows);
+        dim3 grid((unsigned)tiles, (unsigned)((rows + rpc - 1) / rpc));
+        Launch Lz = make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, (int)rpc, ns,
+                                k, loss, top, bot, up, dn);
+        Lz.smem = smem;
+        out.push_back(Lz);
+        break;
+      }
+      default: {
+        const void *fn = d3 ? (const void *)ib::k_hotspot<T, true> : (const void *)ib::k_hotspot<T, false>;
+        const int rpc = hotspot_rows_per_chunk(c, rows);
+        dim3 grid((unsigned)((plane + 255) / 256), (unsigned)((rows + rpc - 1) / rpc));
+        out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, rpc, k,
+                                  loss, top, bot, up, dn));
+      }
+    }
+  }
+}
+
+// Fused leapfrog (k_fdtd_lf): TJ y-rows per tile, NS-stage bulk-copy ring. The largest TJ (and
+// then NS) whose ring lets two CTAs share an SM; the grid is one wave of resident CTAs and the
+// (tile, plane) units are split evenly over it. IB_FDTD_TJ / IB_FDTD_STAGES override.
+struct LfConfig {
+  int tj = 0, ns = 0;
+  size_t smem = 0;
+};
+inline size_t lf_smem(int tj, int ns, int64_t P, int es) {
+  return (size_t)ns * (size_t)(3 * (tj + 2) + 3 * (tj + 1)) * (size_t)P * es + (size_t)ns * 8;
+}
+inline int lf_threads(const ib_ctx *c, int tj) {  // one thread per (row, 16-byte group)
+  const int64_t groups = c->lat_pitch / (16 / c->esize);
+  return (int)(((tj + 1) * groups + 31) / 32 * 32);
+}
+inline LfConfig lf_config(const ib_ctx *c) {
+  // The kernel is bound by the bytes each SM keeps in flight, CTAs/SM x (NS-1) x stage bytes.
+  // Measured at 256^3 binary32 (us/iter): TJ=4/NS=6/1 per SM 130.7, TJ=4/NS=5 137.3,
+  // TJ=3/NS=4/2 per SM 138.5, TJ=3/NS=3/2 per SM 196, TJ=4/NS=3/2 per SM 171. So: 4-row tiles
+  // with the deepest ring one CTA per SM holds (<= 6 stages), then 2 per SM, then smaller tiles.
+  const int64_t P = c->lat_pitch;
+  const int es = c->esize;
+  const size_t cap = 227 * 1024, half = 113 * 1024;
+  LfConfig cfg;
+  const int64_t ftj = env_int("IB_FDTD_TJ", 0), fns = env_int("IB_FDTD_STAGES", 0);
+  const struct { int tj; bool two; } order[] = {{4, false}, {3, true}, {4, true}, {2, true},
+                                                 {3, false}, {2, false}, {1, true}, {1, false}};
+  for (auto o : order) {
+    if (ftj > 0 && o.tj != ftj) continue;
+    if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
+    for (int ns = 3; ns <= 8; ++ns) {
+      if (fns > 0 && ns != fns) continue;
+      const size_t sm = lf_smem(o.tj, ns, P, es);
+      if (sm <= (o.two ? half : cap) && (fns > 0 || ns <= 6)) cfg = {o.tj, ns, sm};
+    }
+    if (cfg.tj && (cfg.ns >= 4 || fns > 0 || ftj > 0)) break;
+    if (cfg.tj && o.tj == 1) break;
+    if (cfg.tj && cfg.ns < 4) cfg = LfConfig{};  // too shallow: try the next shape
+  }
+  if (!cfg.tj) {  // nothing deep enough: take any shape that fits
+    for (auto o : order) {
+      if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
+      const size_t sm = lf_smem(o.tj, 3, P, es);
+      if (sm <= cap) { cfg = {o.tj, 3, sm}; break; }
+    }
+  }
+  return cfg;
+}
+
+template <typename T, bool U, int M>
+const void *lf_fn_m(int tj) {
+  switch (tj) {
+    case 1: return (const void *)ib::k_fdtd_lf<T, U, 1, M>;
+    case 2: return (const void *)ib::k_fdtd_lf<T, U, 2, M>;
+    case 3: return (const void *)ib::k_fdtd_lf<T, U, 3, M>;
+    default: return (const void *)ib::k_fdtd_lf<T, U, 4, M>;
+  }
+}
+template <typename T>
+const void *lf_fn(bool unit, int tj, int mode) {
+  if (unit) return mode == ib::kLfH ? lf_fn_m<T, true, ib::kLfH>(tj)
+                   : mode == ib::kLfE ? lf_fn_m<T, true, ib::kLfE>(tj) : lf_fn_m<T, true, ib::kLfFused>(tj);
+  return mode == ib::kLfH ? lf_fn_m<T, false, ib::kLfH>(tj)
+         : mode == ib::kLfE ? lf_fn_m<T, false, ib::kLfE>(tj) : lf_fn_m<T, false, ib::kLfFused>(tj);
+}
+
+// One k_fdtd_lf launch of `mode` from lattice buffer `from` to `to` (equal for the in-place
+// half-steps).
+template <typename T>
+Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int64_t fs, void *halo_h = nullptr,
+                 int64_t fs_h = 0, void *halo_e = nullptr, int64_t fs_e = 0, int slab = 0) {
+  const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
+  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
+  const bool unit = c->scalars[0] == 1.0;
+  const LfConfig cfg = lf_config(c);
+  const void *fn = lf_fn<T>(unit, cfg.tj, mode);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+  const int threads = lf_threads(c, cfg.tj);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, cfg.smem);
+  // Lockstep (tile, x-chunk) grid: as many x-chunks as the resident slots hold whole columns of
+  // TJ-row tiles (256^3, TJ=4, 148 slots: 65 tiles x 2 chunks). Filling the spare slots with
+  // shorter tiles (74 tiles of 3-4 rows x 2) measured slower (137 vs 131 us): more halo rows.
+  // IB_FDTD_TILES (uneven rows, h <= TJ), IB_FDTD_CHUNKS, IB_FDTD_CTAS (even split) override.
+  const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
+  const int64_t min_tiles = (ny + 1 + cfg.tj - 1) / cfg.tj;
+  int64_t tiles = min_tiles;
+  if (env_int("IB_FDTD_TILES", 0) >= min_tiles) tiles = std::min<int64_t>(ny + 1, env_int("IB_FDTD_TILES", 0));
+  int64_t chunks = env_int("IB_FDTD_CHUNKS", 0);
+  if (chunks <= 0) chunks = std::max<int64_t>(1, slots / tiles);
+  chunks = std::min<int64_t>(chunks, npl);  // every chunk non-empty
+  int64_t ctas = env_int("IB_FDTD_CTAS", 0);
+  if (ctas <= 0) {
+    ctas = tiles * chunks;  // one CTA per (tile, chunk): the kernel maps blockIdx.x to both
+  } else {
+    chunks = 0;  // even split of the tile-major unit list over `ctas` CTAs
+    ctas = std::max<int64_t>(1, std::min(ctas, tiles * npl));
+  }
+  Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), slab, (const T *)from, (T *)to, nx,
+                         ny, nz, (int)c->lat_pitch, fs, x0, npl, (int)tiles, (int)chunks, cfg.ns, ch, ce, d,
+                         (T *)halo_h, fs_h, (T *)halo_e, fs_e);
+  L.smem = cfg.smem;
+  L.step = mode == ib::kLfE ? 1 : 0;
+  return L;
+}
+
+// FDTD, the reference's two half-steps (H then E, in place on the lattice): k_fdtd_lf in its H
+// and E modes, or the lean one-thread-per-point kernels when the z rows are too long for the
+// staged kernel's CTA (or IB_FDTD_KERNEL=lean).
+template <typename T>
+void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
+  const char *force = env_str("IB_FDTD_KERNEL");
+  const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0;
+  const int nx = (int)c->dims[0];
+  const int P = (int)c->slabs.size();
+  if (c->dist()) {  // one rank's slab; the neighbours' halo planes through IPC mappings
+    const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lattice_pitch();
+    Slab &s = c->slabs[0];
+    T *base = (T *)s.buf[0] + (int64_t)(1 - s.row_lo) * plane;
+    void *hh = nullptr, *he = nullptr;
+    int64_t fh = 0, fe = 0;
+    if (c->peer && s.has_bot) {
+      hh = c->peer_buf_dn[0];  // the down rank's top halo plane (its local 0)
+      fh = (int64_t)(c->peer_rows_dn + 2) * plane;
+    }
+    if (c->peer && s.has_top) {
+      he = (T *)c->peer_buf_up[0] + (int64_t)(c->peer_rows_up + 1) * plane;  // the up rank's bottom halo
+      fe = (int64_t)(c->peer_rows_up + 2) * plane;
+    }
+    out.push_back(lf_launch<T>(c, ib::kLfH, base, base, s.row_lo, s.rows(), s.fs, hh, fh, nullptr, 0, 0));
+    out.push_back(lf_launch<T>(c, ib::kLfE, base, base, s.row_lo, s.rows(), s.fs, nullptr, 0, he, fe, 0));
+    return;
+  }
+  if (P > 1) {  // axis-0 slabs: every H launch, then every E launch, halo planes pushed in-kernel
+    const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lat_pitch;
+    for (int step = 0; step < 2; ++step)
+      for (int g = 0; g < P; ++g) {
+        Slab &s = c->slabs[g];
+        T *base = (T *)s.buf[0] + (int64_t)(1 - s.row_lo) * plane;  // global plane index -> buffer
+        void *hh = nullptr, *he = nullptr;
+        int64_t fh = 0, fe = 0;
+        if (step == 0 && g + 1 < P) {
+          hh = c->slabs[g + 1].buf[0];  // its top halo plane (local 0)
+          fh = c->slabs[g + 1].fs;
+        }
+        if (step == 1 && g > 0) {
+          Slab &n = c->slabs[g - 1];
+          he = (T *)n.buf[0] + (int64_t)(n.rows() + 1) * plane;  // its bottom halo plane
+          fe = n.fs;
+        }
+        out.push_back(lf_launch<T>(c, step == 0 ? ib::kLfH : ib::kLfE, base, base, s.row_lo, s.rows(), s.fs,
+                                   hh, fh, he, fe, g));
+      }
+    return;
+  }
+  if (!lean) {
+    out.push_back(lf_launch<T>(c, ib::kLfH, c->lat[0], c->lat[0], 0, nx + 1, c->lat_fs));
+    out.push_back(lf_launch<T>(c, ib::kLfE, c->lat[0], c->lat[0], 0, nx + 1, c->lat_fs));
+    return;
+  }
+  const int ny = (int)c->dims[1], nz = (int)c->dims[2];
+  const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
+  const bool unit = c->scalars[0] == 1.0;
+  dim3 b2(32, 8);
+  dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)(nx + 1));
+  const void *fh = unit ? (const void *)ib::k_fdtd_h2<T, true> : (const void *)ib::k_fdtd_h2<T, false>;
+  const void *fe = unit ? (const void *)ib::k_fdtd_e2<T, true> : (const void *)ib::k_fdtd_e2<T, false>;
+  T *f = (T *)c->lat[0];
+  out.push_back(make_launch(fh, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ch, d));
+  out.push_back(make_launch(fe, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ce, d));
+  out.back().step = 1;
+}
+
+// FDTD fused: one k_fdtd_lf launch per iteration, parity -> parity ^ 1.
+template <typename T>
+void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1], 0, (int)c->dims[0] + 1,
+                             c->lat_fs));
+}
+
+void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
+  out.clear();
+  switch (c->solver) {
+    case IB_SOLVER_VECTOR: {
+      const int64_t n = c->dims[0];
+      const double cc = c->scalars[0];
+      // 128-thread CTAs measured best (1.21 / 1.23 / 1.24 / 1.40 us per iteration in a PDL graph at
+      // 128 / 256 / 512 / 1024); IB_VECTOR_BLOCK overrides
+      int64_t bs = env_int("IB_VECTOR_BLOCK", 128);
+      bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
+      if (c->dtype == IB_F32) {
+        const int64_t threads = (n >> 2) + (n & 3);
+        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
+        out.push_back(make_launch((const void *)ib::k_vector_f32, grid, block, 0,
+                                  (float *)c->field[0], n, cc));
+      } else {
+        const int64_t threads = (n >> 1) + (n & 1);
+        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
+        out.push_back(make_launch((const void *)ib::k_vector_f64, grid, block, 0,
+                                  (double *)c->field[0], n, cc));
+      }
+      break;
+    }
+    case IB_SOLVER_HOTSPOT2D:
+    case IB_SOLVER_HOTSPOT3D:
+      if (c->dtype == IB_F32)
+        hotspot_launches<float>(c, parity, out);
+      else
+        hotspot_launches<double>(c, parity, out);
+      break;
+    case IB_SOLVER_FDTD:
+      if (c->dtype == IB_F32)
+        fdtd_launches<float>(c, out);
+      else
+        fdtd_launches<double>(c, out);
+      break;
+    case IB_SOLVER_FDTD_FUSED:
+      if (c->dtype == IB_F32)
+        fdtd_fused_launches<float>(c, parity, out);
+      else
+        fdtd_fused_launches<double>(c, parity, out);
+      break;
+  }
+}
+
+}  // namespace

@@ -1,8 +1,11 @@
 import os, sys, statistics
 sys.path.insert(0, os.getcwd())
 from paper_2501_09398_b200 import cli, workloads as wl
-cases = [("hotspot2d", [1024], 2000, [(2, 256), (2, 512), (1, 512)]),
-         ("hotspot3d", [512, 8], 1000, [(2, 128), (2, 256), (4, 512), (4, 256)])]
+import json
+cases = json.loads(os.environ.get("CASES", "null")) or [
+    ("hotspot2d", [1024], 2000, [(2, 256), (2, 512), (1, 512)]),
+    ("hotspot3d", [512, 8], 1000, [(2, 128), (2, 256), (4, 512), (4, 256)])]
+cases = [(w, size, n, [tuple(v) for v in vs]) for w, size, n, vs in cases]
 for w, size, n, vs in cases:
     st = cli.build_workload(w, size)
     res = {v: [] for v in vs}
@@ -15,7 +18,7 @@ for w, size, n, vs in cases:
             xs = []
             for _ in range(5):
                 s.flush_l2(); s.upload(st)
-                xs.append(s.run_batched(50, n // 50, pdl=True).gpu_s / n)
+                xs.append(s.run_batched(50, n // 50, pdl=os.environ.get("PDL", "1") == "1").gpu_s / n)
             res[(r, bs)].append(1e6 * statistics.median(xs))
             s.close()
     for v, xs in res.items():
