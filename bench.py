@@ -596,6 +596,7 @@ def run_ours(args, dist: Dist) -> int:
         },
         "speedup_vs_stream": round(head["speedup_vs_stream"], 3),
         "stream_us_per_iter": round(head["stream_us_per_iter"], 4),
+        "stream_pdl_us_per_iter": round(head["stream_pdl_us_per_iter"], 4),
         "graph_exec_us_per_iter": round(head["graph_exec_us_per_iter"], 4),
         "T_C_us": round(head["T_C_us"], 1),
         "roofline": head["roofline"],
