@@ -588,7 +588,10 @@ __global__ void __launch_bounds__(256)
 // ================================================================================================
 // (TJ+1) x groups-per-row threads, rounded up to warps; two CTAs per SM must fit the register file.
 // (TJ = 6 / 8 with one CTA per SM measured no faster than TJ = 4: 141.6 / 212.9 vs 142.6 us fused.)
+// binary64 rows hold half as many elements per 16-byte group, so a tile row needs twice the
+// threads: up to 704 (4-row tiles, one CTA per SM).
 constexpr int kLfMaxThreads = 384;
+constexpr int lf_max_threads(int esize) { return esize == 8 ? 704 : kLfMaxThreads; }
 // MODE: kLfFused (above), kLfH / kLfE = the H or the E half-step alone, in place (src == dst),
 // the two-launch leapfrog of the reference's program (workloads.py:325-413). Same staging and
 // march; H alone skips the seed plane and the E phase, E alone loads H instead of computing it and
@@ -598,7 +601,7 @@ constexpr int kLfMaxThreads = 384;
 constexpr int kLfFused = 0, kLfH = 1, kLfE = 2;
 
 template <typename T, bool UNIT_D, int TJ, int MODE>
-__global__ void __launch_bounds__(ib::kLfMaxThreads, 2)
+__global__ void __launch_bounds__(ib::lf_max_threads(sizeof(T)), sizeof(T) == 8 ? 1 : 2)
     k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int x0, int npl, int tiles,
               int chunks, int nstages, T c_h, T c_e, T d, T *halo_h, int64_t fs_h, T *halo_e,
               int64_t fs_e) {

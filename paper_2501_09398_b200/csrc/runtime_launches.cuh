@@ -204,37 +204,32 @@ inline int lf_threads(const ib_ctx *c, int tj) {  // one thread per (row, 16-byt
   return (int)(((tj + 1) * groups + 31) / 32 * 32);
 }
 inline LfConfig lf_config(const ib_ctx *c) {
-  // The kernel is bound by the bytes each SM keeps in flight, CTAs/SM x (NS-1) x stage bytes.
-  // Measured at 256^3 binary32 (us/iter): TJ=4/NS=6/1 per SM 130.7, TJ=4/NS=5 137.3,
-  // TJ=3/NS=4/2 per SM 138.5, TJ=3/NS=3/2 per SM 196, TJ=4/NS=3/2 per SM 171. So: 4-row tiles
-  // with the deepest ring one CTA per SM holds (<= 6 stages), then 2 per SM, then smaller tiles.
+  // The kernel is bound by how much each SM keeps in flight, and the ring depth in planes counts
+  // more than its bytes. Measured at 256^3 (us/iter) binary32: TJ=4/NS=6 one CTA per SM 130.7,
+  // TJ=4/NS=5 137.3, TJ=3/NS=4 two per SM 138.5, TJ=3/NS=3 196, TJ=4/NS=3 171; binary64 (twice
+  // the threads per row): TJ=2/NS=5 fused 300.6 / two half-steps 383.4, TJ=3/NS=4 364 / 480,
+  // TJ=4/NS=3 433 / 486. So: the first shape (largest tiles, one CTA per SM first) whose ring
+  // holds >= 5 stages, else >= 4, else any. IB_FDTD_TJ / IB_FDTD_STAGES force a shape.
   const int64_t P = c->lat_pitch;
   const int es = c->esize;
   const size_t cap = 227 * 1024, half = 113 * 1024;
-  LfConfig cfg;
   const int64_t ftj = env_int("IB_FDTD_TJ", 0), fns = env_int("IB_FDTD_STAGES", 0);
   const struct { int tj; bool two; } order[] = {{4, false}, {3, true}, {4, true}, {2, true},
                                                  {3, false}, {2, false}, {1, true}, {1, false}};
-  for (auto o : order) {
-    if (ftj > 0 && o.tj != ftj) continue;
-    if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
-    for (int ns = 3; ns <= 8; ++ns) {
-      if (fns > 0 && ns != fns) continue;
-      const size_t sm = lf_smem(o.tj, ns, P, es);
-      if (sm <= (o.two ? half : cap) && (fns > 0 || ns <= 6)) cfg = {o.tj, ns, sm};
-    }
-    if (cfg.tj && (cfg.ns >= 4 || fns > 0 || ftj > 0)) break;
-    if (cfg.tj && o.tj == 1) break;
-    if (cfg.tj && cfg.ns < 4) cfg = LfConfig{};  // too shallow: try the next shape
-  }
-  if (!cfg.tj) {  // nothing deep enough: take any shape that fits
+  for (int min_ns : {5, 4, 3}) {
     for (auto o : order) {
-      if (lf_threads(c, o.tj) > ib::kLfMaxThreads) continue;
-      const size_t sm = lf_smem(o.tj, 3, P, es);
-      if (sm <= cap) { cfg = {o.tj, 3, sm}; break; }
+      if (ftj > 0 && o.tj != ftj) continue;
+      if (lf_threads(c, o.tj) > ib::lf_max_threads(es)) continue;
+      LfConfig cfg;
+      for (int ns = 3; ns <= (fns > 0 ? 8 : 6); ++ns) {
+        if (fns > 0 && ns != fns) continue;
+        const size_t sm = lf_smem(o.tj, ns, P, es);
+        if (sm <= (o.two ? half : cap)) cfg = {o.tj, ns, sm};
+      }
+      if (cfg.tj && (cfg.ns >= min_ns || fns > 0)) return cfg;
     }
   }
-  return cfg;
+  return LfConfig{};
 }
 
 template <typename T, bool U, int M>
