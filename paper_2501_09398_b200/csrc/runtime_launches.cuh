@@ -221,7 +221,7 @@ inline LfConfig lf_config(const ib_ctx *c) {
       if (ftj > 0 && o.tj != ftj) continue;
       if (lf_threads(c, o.tj) > ib::lf_max_threads(es)) continue;
       LfConfig cfg;
-      for (int ns = 3; ns <= (fns > 0 ? 8 : 6); ++ns) {
+      for (int ns = 3; ns <= (fns > 0 ? 12 : 6); ++ns) {
         if (fns > 0 && ns != fns) continue;
         const size_t sm = lf_smem(o.tj, ns, P, es);
         if (sm <= (o.two ? half : cap)) cfg = {o.tj, ns, sm};
