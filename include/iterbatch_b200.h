@@ -187,6 +187,9 @@ int ib_slab_info(const ib_ctx *ctx, int64_t *lo, int64_t *hi, int *has_top, int 
  * processes is a pair of one-thread kernels per iteration (wait for the neighbours' completed-
  * iteration counters, publish this rank's), all inside the iteration-batch graph. A lost
  * neighbour traps after IB_DIST_TIMEOUT_MS (default 20000) instead of hanging the device.
+ * A neighbour's first kernel of a run stores into this rank's halo planes, so the ranks must
+ * synchronise (any host barrier) after ib_upload and before the next run; a run itself ends only
+ * once the neighbours are done, so downloads need no barrier.
  * Replaces the NCCL group of ib_create_dist(id128 != NULL). SURVEY.md §8e, v2. */
 #define IB_IPC_BYTES 192
 int ib_ipc_export(const ib_ctx *ctx, void *out, size_t bytes);

@@ -133,7 +133,8 @@ class DistributedSolver(DeviceSolver):
         _lib.check(L.ib_create_dist(ctypes.byref(ctx), _lib.SOLVER[kind], _lib.DTYPE[self.dtype], dims,
                                     len(self.dims), sc, len(self.scalars), device, rank, world, idp))
         self._ctx = ctx
-        if world > 1 and exchange == "peer":
+        self._allgather = allgather if (world > 1 and exchange == "peer") else None
+        if self._allgather is not None:
             self._attach_peers(allgather)
         if kind == "fdtd":
             self.nfields = 6
@@ -212,6 +213,10 @@ class DistributedSolver(DeviceSolver):
                 continue
             a = np.ascontiguousarray(a, dtype=self.np_dtype)
             _lib.check(L.ib_upload(self.ctx, f, a.ctypes.data_as(ctypes.c_void_p), a.nbytes))
+        if self._allgather is not None:
+            # peer exchange: a neighbour's first kernel stores into this rank's halo planes, so
+            # no rank may start running before every rank's upload has landed (host barrier)
+            self._allgather(b"")
 
     def build_graph(self, batch_size: int, build: str = "capture", pdl: bool = False,
                     device_launch: bool = False, upload: bool = True,
