@@ -269,6 +269,7 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
         stream_mean = statistics.fmean(stream_s)
         exec_mean = statistics.fmean(exec_s)
         it_bytes = solver.iteration_bytes
+        state_bytes = sum(a.nbytes for a in solver.host_arrays(state))
         peak, peak_src = measured_peaks()
         achieved = it_bytes / (exec_mean / n) / 1e9
         kpi = solver.kernels_per_iteration
@@ -293,7 +294,10 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(name),
                 "bytes_per_iter": it_bytes, "peak_source": peak_src,
                 "note": "per-iteration algorithmic bytes / per-iteration graph execution time"
-                        + ("; fused FDTD: each field read+written once = 48 B/cell" if cfg.get("fuse") else ""),
+                        + ("; fused FDTD: each field read+written once = 48 B/cell" if cfg.get("fuse") else "")
+                        + ("; the state (%.1f MB) stays L2-resident across iterations, so this per-launch "
+                           "kernel is launch/latency-bound and the HBM roof is not the binding one "
+                           "(DESIGN.md §4)" % (state_bytes / 1e6) if state_bytes < (96 << 20) else ""),
             },
             "k_sweep": sweep,
             "clocks": clocks.summary(),
