@@ -269,7 +269,7 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
         stream_mean = statistics.fmean(stream_s)
         exec_mean = statistics.fmean(exec_s)
         it_bytes = solver.iteration_bytes
-        state_bytes = sum(a.nbytes for a in solver.host_arrays(state))
+        state_bytes = sum(int(np.prod(shp)) for shp in solver.shapes) * np.dtype(solver.np_dtype).itemsize
         peak, peak_src = measured_peaks()
         achieved = it_bytes / (exec_mean / n) / 1e9
         kpi = solver.kernels_per_iteration
