@@ -29,6 +29,7 @@ san() {  # tool workload size dtype [extra profile_run args]
 for tool in memcheck racecheck; do
   san $tool hotspot2d 64,48 f32; san $tool hotspot3d 24,20,8 f64; san $tool fdtd 9,5,7 f32; san $tool vector 1001 f32
   san $tool fdtd 9,5,7 f32 --fuse; san $tool fdtd 20,17,40 f64 --fuse; IB_FDTD_KERNEL=lean san $tool fdtd 9,5,7 f32
+  san $tool hotspot2d 40,128 f32; san $tool hotspot3d 24,16,8 f32; san $tool hotspot3d 24,16,8 f64  # shuffle paths
   IB_HOTSPOT_KERNEL=tma san $tool hotspot3d 40,16,256 f32
 done
 IB_HOTSPOT_KERNEL=tma san synccheck hotspot3d 40,16,256 f32
