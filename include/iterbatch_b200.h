@@ -95,9 +95,14 @@ int ib_mem_info(int device, int64_t *free_bytes, int64_t *total_bytes);
  *          Constants are passed in binary64 and rounded ONCE to the state dtype on the host,
  *          except the vector constant in IB_F32 which stays binary64 (v' = (float)((double)v*c)).
  * devices: one entry per slab; hotspot solvers partition axis 0 into ndevices slabs with the
- *          reference's bounds formula rows*g//P (workloads.py:65). Device ids may repeat (several
- *          slabs on one GPU: the halo exchange then goes through local memory, same graph).
- *          vector / fdtd require ndevices == 1. NULL/0 means {current device}.
+ *          reference's bounds formula rows*g//P (workloads.py:65), IB_SOLVER_FDTD partitions the
+ *          (nx+1)-plane lattice the same way. Each slab's kernel stores its boundary plane(s)
+ *          straight into the neighbours' halo planes (peer pointers between devices); cross-slab
+ *          ordering is graph edges. Device ids may repeat (several slabs on one GPU, same graph).
+ *          vector / fused fdtd require ndevices == 1. NULL/0 means {current device}.
+ * Device layout: vector and hotspot fields are C-order like the reference's arrays; both FDTD
+ *          solvers keep the six fields on one padded (nx+1) x (ny+1) x P lattice (P = nz+1
+ *          rounded up to 16 bytes), converted by ib_upload / ib_download.
  */
 int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
               const double *scalars, int nscalars, const int *devices, int ndevices);
