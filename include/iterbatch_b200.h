@@ -62,6 +62,10 @@ extern "C" {
                                      runs all num_batches batches (device-side loop, no host gap) */
 #define IB_FLAG_MEMINFO 0x10      /* fill ib_times.graph_bytes from cudaMemGetInfo before/after the
                                      build (the paper's m_base/m_node probe; costs ~ms per call) */
+#define IB_FLAG_PATCH 0x20        /* odd batch_size on a ping-pong solver: ONE executable whose kernel
+                                     nodes are re-pointed (cudaGraphExecKernelNodeSetParams) before a
+                                     launch that starts on the other buffer parity, instead of a second
+                                     executable with the parity baked in (manual builds, one slab) */
 
 /* Per-call timing record. Host times are steady-clock seconds; gpu_s is CUDA-event time on the
  * context's launch stream (first launch .. end of last kernel). */

@@ -17,7 +17,7 @@ IB_OK, IB_EINVAL, IB_ECUDA, IB_ENOMEM, IB_ESTATE, IB_ENODEV = 0, -1, -2, -3, -4,
 SOLVER = {"vector": 0, "hotspot2d": 1, "hotspot3d": 2, "fdtd": 3, "fdtd_fused": 4}
 DTYPE = {"f32": 0, "f64": 1}
 BUILD = {"manual": 0, "capture": 1}
-FLAG_PDL, FLAG_DEVICE_LAUNCH, FLAG_NO_UPLOAD, FLAG_WHILE, FLAG_MEMINFO = 0x1, 0x2, 0x4, 0x8, 0x10
+FLAG_PDL, FLAG_DEVICE_LAUNCH, FLAG_NO_UPLOAD, FLAG_WHILE, FLAG_MEMINFO, FLAG_PATCH = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 
 FNV_OFFSET = 0xCBF29CE484222325
 

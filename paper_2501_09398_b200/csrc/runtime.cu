@@ -688,8 +688,23 @@ int ib_graph_build(ib_ctx *c, int64_t batch_size, int build_mode, int flags, ib_
   size_t f0 = 0, f1 = 0, tot = 0;
   const bool meminfo = (flags & IB_FLAG_MEMINFO) != 0;
   if (meminfo) IB_CUDA(cudaMemGetInfo(&f0, &tot));
-  int rc = build_one(c, c->cur, &t);
-  if (rc == IB_OK && c->ping_pong() && (batch_size & 1)) rc = build_one(c, c->cur ^ 1, &t);
+  const bool patch = (flags & IB_FLAG_PATCH) != 0;
+  if (patch && (build_mode != IB_BUILD_MANUAL || c->slabs.size() > 1 || c->dist() || (flags & IB_FLAG_WHILE)))
+    return fail(IB_EINVAL, "IB_FLAG_PATCH needs a manual build on one slab, without IB_FLAG_WHILE");
+  int rc;
+  if (patch) {  // one executable (in exec[0]) built at the current parity, re-pointed as needed
+    rc = build_one(c, c->cur, &t);
+    if (rc == IB_OK && c->cur != 0) {
+      c->exec[0] = c->exec[c->cur];
+      c->graph[0] = c->graph[c->cur];
+      c->exec[c->cur] = nullptr;
+      c->graph[c->cur] = nullptr;
+    }
+    c->exec_parity = c->cur;
+  } else {
+    rc = build_one(c, c->cur, &t);
+    if (rc == IB_OK && c->ping_pong() && (batch_size & 1)) rc = build_one(c, c->cur ^ 1, &t);
+  }
   if (rc != IB_OK) {
     std::string msg = g_err;
     free_graphs(c);
@@ -713,9 +728,10 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
   IB_CUDA(cudaSetDevice(c->slabs[0].device));
   IB_TRY(sync_all(c));
   ib_times t = {};
+  const bool patch = (c->gflags & IB_FLAG_PATCH) != 0;
   // the state parity may have moved since the build (e.g. an odd stream run): build lazily
-  if (!c->exec[c->cur]) IB_TRY(build_one(c, c->cur, &t));
-  if (c->ping_pong() && (c->K & 1) && !c->exec[c->cur ^ 1]) IB_TRY(build_one(c, c->cur ^ 1, &t));
+  if (!patch && !c->exec[c->cur]) IB_TRY(build_one(c, c->cur, &t));
+  if (!patch && c->ping_pong() && (c->K & 1) && !c->exec[c->cur ^ 1]) IB_TRY(build_one(c, c->cur ^ 1, &t));
   const bool wh = (c->gflags & IB_FLAG_WHILE) != 0;
   const int64_t per = c->K * (c->solver == IB_SOLVER_FDTD ? 2 : 1) * (int64_t)c->slabs.size();  // kernels / batch
   auto a = clk::now();
@@ -733,7 +749,12 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
     } else {
       for (int64_t b = 0; b < num_batches; ++b) {
         c->ev(IB_EV_GRAPH_LAUNCHED, b);
-        IB_CUDA(cudaGraphLaunch(c->exec[c->cur], c->stream()));
+        if (patch) {
+          if (c->ping_pong() && c->exec_parity != c->cur) IB_TRY(patch_exec_parity(c, c->cur));
+          IB_CUDA(cudaGraphLaunch(c->exec[0], c->stream()));
+        } else {
+          IB_CUDA(cudaGraphLaunch(c->exec[c->cur], c->stream()));
+        }
         if (c->ping_pong() && (c->K & 1)) c->cur ^= 1;
       }
       t.launches = num_batches;

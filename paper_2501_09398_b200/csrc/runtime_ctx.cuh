@@ -26,6 +26,10 @@ struct ib_ctx {
   int gflags = 0, gmode = 0;
   cudaGraph_t graph[2] = {nullptr, nullptr};
   cudaGraphExec_t exec[2] = {nullptr, nullptr};  // indexed by start parity
+  // IB_FLAG_PATCH: the single executable's kernel nodes in chain order, and the start parity its
+  // node parameters currently encode
+  std::vector<cudaGraphNode_t> kernel_nodes;
+  int exec_parity = 0;
   cudaGraphConditionalHandle cond[2] = {};
   int *d_counter = nullptr;  // WHILE-mode remaining-batch counter
   void *flush = nullptr;

@@ -134,6 +134,27 @@ int join_into(ib_ctx *c, cudaStream_t root, bool fork) {
   return IB_OK;
 }
 
+// IB_FLAG_PATCH: re-point the single executable's kernel nodes so it starts at `parity`.
+int patch_exec_parity(ib_ctx *c, int parity) {
+  std::vector<Launch> its[2];
+  iteration_launches(c, 0, its[0]);
+  iteration_launches(c, 1, its[1]);
+  const size_t per = its[0].size();
+  for (size_t n = 0; n < c->kernel_nodes.size(); ++n) {
+    const int64_t t = (int64_t)(n / per);
+    Launch &L = its[(parity + t) & 1][n % per];
+    cudaKernelNodeParams np = {};
+    np.func = const_cast<void *>(L.func);
+    np.gridDim = L.grid;
+    np.blockDim = L.block;
+    np.sharedMemBytes = (unsigned)L.smem;
+    np.kernelParams = L.args();
+    IB_CUDA(cudaGraphExecKernelNodeSetParams(c->exec[0], c->kernel_nodes[n], &np));
+  }
+  c->exec_parity = parity;
+  return IB_OK;
+}
+
 void free_graphs(ib_ctx *c) {
   for (int p = 0; p < 2; ++p) {
     if (c->exec[p]) cudaGraphExecDestroy(c->exec[p]);
@@ -141,6 +162,7 @@ void free_graphs(ib_ctx *c) {
     c->exec[p] = nullptr;
     c->graph[p] = nullptr;
   }
+  c->kernel_nodes.clear();
   c->K = 0;
 }
 
@@ -177,6 +199,7 @@ int build_manual_chain(ib_ctx *c, cudaGraph_t graph, int64_t K, int parity, bool
         IB_CUDA(cudaGraphAddDependencies_v2(graph, &prev, &node, &ed, 1));
       }
       prev = node;
+      if (c->gflags & IB_FLAG_PATCH) c->kernel_nodes.push_back(node);
       c->ev(IB_EV_NODE_ADDED, -1, *nodes);
       ++*nodes;
     }

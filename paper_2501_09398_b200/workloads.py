@@ -437,7 +437,7 @@ class DeviceSolver:
 
     def build_graph(self, batch_size: int, build: str = "manual", pdl: bool = False,
                     device_launch: bool = False, upload: bool = True,
-                    while_loop: bool = False, meminfo: bool = False) -> Times:
+                    while_loop: bool = False, meminfo: bool = False, patch: bool = False) -> Times:
         """Unroll batch_size iterations into a graph, instantiate and upload it (T_C).
 
         ``meminfo`` also records the device memory the instantiated graph(s) took
@@ -448,7 +448,7 @@ class DeviceSolver:
             raise ValueError(f"build must be one of {sorted(_lib.BUILD)}, got {build!r}")
         flags = ((_lib.FLAG_PDL if pdl else 0) | (_lib.FLAG_DEVICE_LAUNCH if device_launch else 0)
                  | (0 if upload else _lib.FLAG_NO_UPLOAD) | (_lib.FLAG_WHILE if while_loop else 0)
-                 | (_lib.FLAG_MEMINFO if meminfo else 0))
+                 | (_lib.FLAG_MEMINFO if meminfo else 0) | (_lib.FLAG_PATCH if patch else 0))
         t = _lib.IbTimes()
         _lib.check(_lib.lib().ib_graph_build(self.ctx, int(batch_size), _lib.BUILD[build], flags,
                                              ctypes.byref(t)))
@@ -456,9 +456,15 @@ class DeviceSolver:
         return Times.from_c(t)
 
     def run_batched(self, batch_size: int, num_batches: int, build: str = "manual",
-                    pdl: bool = False, while_loop: bool = False) -> Times:
-        """Build + replay + destroy in one call; ``gpu_s`` is T = T_C + T_E on the device clock."""
-        flags = (_lib.FLAG_PDL if pdl else 0) | (_lib.FLAG_WHILE if while_loop else 0)
+                    pdl: bool = False, while_loop: bool = False, patch: bool = False) -> Times:
+        """Build + replay + destroy in one call; ``gpu_s`` is T = T_C + T_E on the device clock.
+
+        ``patch``: an odd batch on a ping-pong solver uses ONE executable whose kernel nodes are
+        re-pointed with cudaGraphExecKernelNodeSetParams between launches, instead of a second
+        executable with the other buffer parity baked in.
+        """
+        flags = ((_lib.FLAG_PDL if pdl else 0) | (_lib.FLAG_WHILE if while_loop else 0)
+                 | (_lib.FLAG_PATCH if patch else 0))
         t = _lib.IbTimes()
         _lib.check(_lib.lib().ib_run_batched(self.ctx, int(batch_size), int(num_batches),
                                              _lib.BUILD[build], flags, ctypes.byref(t)))
@@ -653,7 +659,7 @@ def run_loop(program, state, total_iterations: int, workers=None, *, dtype="f64"
 
 def run_batched(program, state, batch_size: int, num_batches: int, workers=None, *, dtype="f64",
                 devices=None, build: str = "manual", pdl: bool = False, while_loop: bool = False,
-                fuse: bool = False):
+                fuse: bool = False, patch: bool = False):
     """Apply the program in num_batches replays of a batch_size-iteration CUDA graph (Listing 3).
 
     Mirrors workloads.py:453-471 (batch_size < 1 or num_batches < 0 raise ValueError) and
@@ -669,7 +675,7 @@ def run_batched(program, state, batch_size: int, num_batches: int, workers=None,
     if num == 0:
         return state
     s = _solver_for(state, dtype, devices, fuse)
-    s.build_graph(size, build=build, pdl=pdl, while_loop=while_loop)
+    s.build_graph(size, build=build, pdl=pdl, while_loop=while_loop, patch=patch)
     s.run_graph(num)
     s.destroy_graph()
     return s.download(state, fields=_written_fields(state))

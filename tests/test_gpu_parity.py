@@ -207,6 +207,30 @@ def test_p3_odd_batch_after_odd_stream_run(gpu):
     s.close()
 
 
+@pytest.mark.parametrize("pdl", [False, True])
+@pytest.mark.parametrize("workload,size", [("hotspot2d", [37, 29]), ("hotspot3d", [20, 16, 8]),
+                                           ("vector", [1001]), ("fdtd", [9, 5, 7])])
+def test_p3_patched_parity_equals_loop(gpu, workload, size, pdl):
+    """IB_FLAG_PATCH: one executable re-pointed with cudaGraphExecKernelNodeSetParams (odd K, and
+    after an odd stream run moved the parity) == the loop, bit for bit; the alternative to the
+    second baked-parity executable (north star: 'baked into the unrolled nodes or patched')."""
+    state = cli.build_workload(workload, size)
+    prog = cli.programs()[workload]()
+    ref = wl.state_checksum(wl.run_loop(prog, state, 3 + 5 * 3 + 5 * 2))
+    s = wl.DeviceSolver(state, "f64")
+    s.run_stream(3)                      # odd: the executable is built at the other parity
+    t = s.build_graph(5, pdl=pdl, patch=True)
+    assert t.nodes == 5 * s.kernels_per_iteration  # one executable, not two
+    s.run_graph(3)
+    s.run_graph(2)
+    assert wl.state_checksum(s.download(state)) == ref
+    s.close()
+    got = wl.run_batched(prog, state, 7, 3, patch=True, dtype="f32")
+    want = wl.run_loop(prog, state, 21, dtype="f32")
+    for g, w in zip(got.state_arrays(), want.state_arrays()):
+        assert np.array_equal(g, w)
+
+
 # ---- per-step API and fixtures -------------------------------------------------------------------
 def test_steps_match_reference_fixtures(gpu, fixtures):
     v = wl.VectorWorkload(fixtures["vector_in"], 0.9999)

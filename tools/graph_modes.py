@@ -10,6 +10,8 @@ can batch iterations (run under gpurun; writes gpurun_out/graph_modes.json and p
   while             the K-chain inside a conditional WHILE node: ONE cudaGraphLaunch for all batches
   while+pdl         both
   peeled N+7        loop peeling: floor(N/K) replays + one remainder graph (N not divisible by K)
+  odd K=25 baked    odd batch on a ping-pong solver: two executables, parity baked into each
+  odd K=25 patched  one executable re-pointed with cudaGraphExecKernelNodeSetParams between launches
 
 Device time (CUDA events) per iteration, L2 flushed before each run, median of 5; T_C is the host
 build time (create + instantiate + upload).
@@ -50,6 +52,15 @@ def main():
                 return r
             return f
 
+        def graph25(**kw):  # odd K on a ping-pong solver: two executables vs one re-pointed one
+            def f():
+                b = s.build_graph(25, pdl=True, **kw)
+                r = s.run_graph(n // 25)
+                s.destroy_graph()
+                r.build_s = b.build_s
+                return r
+            return f
+
         modes = [
             ("stream", lambda: s.run_stream(n)),
             ("stream+pdl", lambda: s.run_stream(n, pdl=True)),
@@ -60,6 +71,8 @@ def main():
             ("while", graph(while_loop=True)),
             ("while+pdl", graph(while_loop=True, pdl=True)),
             ("peeled N+7", lambda: s.run_peeled(n + 7, k)),
+            ("odd K=25 baked", graph25()),
+            ("odd K=25 patched", graph25(patch=True)),
         ]
         timed(modes[2][1])  # warm-up
         for name, fn in modes:
