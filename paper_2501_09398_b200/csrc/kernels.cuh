@@ -43,36 +43,45 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 //             rounding c=0.9999 to binary32 drifts 1.7e-4 over 10^4 steps; this form 2.5e-6).
 // Launch: one float4 / double2 per thread; a scalar tail handles n % 4 (n % 2).
 // ================================================================================================
+// Grid-stride over the (n/4 groups + n%4 tail) work items: the launch layer caps the grid at a few
+// waves for large n (CTA dispatch would otherwise dominate: 131K CTAs for 2^26 elements) and uses
+// one item per thread for the launch-bound small sizes.
+template <bool LOOP>
 __global__ void __launch_bounds__(1024) k_vector_f32(float *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n4 = n >> 2;
-  if (i < n4) {
-    float4 a = reinterpret_cast<float4 *>(v)[i];
-    a.x = (float)__dmul_rn((double)a.x, c);
-    a.y = (float)__dmul_rn((double)a.y, c);
-    a.z = (float)__dmul_rn((double)a.z, c);
-    a.w = (float)__dmul_rn((double)a.w, c);
-    reinterpret_cast<float4 *>(v)[i] = a;
-  } else {
-    const int64_t t = (n4 << 2) + (i - n4);
-    if (i - n4 < (n & 3) && t < n) v[t] = (float)__dmul_rn((double)v[t], c);
+  const int64_t n4 = n >> 2, items = n4 + (n & 3);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < items;
+       i += LOOP ? (int64_t)gridDim.x * blockDim.x : items) {
+    if (i < n4) {
+      float4 a = reinterpret_cast<float4 *>(v)[i];
+      a.x = (float)__dmul_rn((double)a.x, c);
+      a.y = (float)__dmul_rn((double)a.y, c);
+      a.z = (float)__dmul_rn((double)a.z, c);
+      a.w = (float)__dmul_rn((double)a.w, c);
+      reinterpret_cast<float4 *>(v)[i] = a;
+    } else {
+      const int64_t t = (n4 << 2) + (i - n4);
+      v[t] = (float)__dmul_rn((double)v[t], c);
+    }
   }
 }
 
+template <bool LOOP>
 __global__ void __launch_bounds__(1024) k_vector_f64(double *__restrict__ v, int64_t n, double c) {
   pdl_trigger();
   pdl_wait();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n2 = n >> 1;
-  if (i < n2) {
-    double2 a = reinterpret_cast<double2 *>(v)[i];
-    a.x = __dmul_rn(a.x, c);
-    a.y = __dmul_rn(a.y, c);
-    reinterpret_cast<double2 *>(v)[i] = a;
-  } else if (i == n2 && (n & 1)) {
-    v[n - 1] = __dmul_rn(v[n - 1], c);
+  const int64_t n2 = n >> 1, items = n2 + (n & 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < items;
+       i += LOOP ? (int64_t)gridDim.x * blockDim.x : items) {
+    if (i < n2) {
+      double2 a = reinterpret_cast<double2 *>(v)[i];
+      a.x = __dmul_rn(a.x, c);
+      a.y = __dmul_rn(a.y, c);
+      reinterpret_cast<double2 *>(v)[i] = a;
+    } else {
+      v[n - 1] = __dmul_rn(v[n - 1], c);
+    }
   }
 }
 
@@ -590,7 +599,7 @@ __global__ void __launch_bounds__(256)
 // (TJ = 6 / 8 with one CTA per SM measured no faster than TJ = 4: 141.6 / 212.9 vs 142.6 us fused.)
 // binary64 rows hold half as many elements per 16-byte group, so a tile row needs twice the
 // threads: up to 704 (4-row tiles, one CTA per SM).
-constexpr int kLfMaxThreads = 384;
+constexpr int kLfMaxThreads = 704;
 constexpr int lf_max_threads(int esize) { return esize == 8 ? 704 : kLfMaxThreads; }
 // MODE: kLfFused (above), kLfH / kLfE = the H or the E half-step alone, in place (src == dst),
 // the two-launch leapfrog of the reference's program (workloads.py:325-413). Same staging and
@@ -601,7 +610,7 @@ constexpr int lf_max_threads(int esize) { return esize == 8 ? 704 : kLfMaxThread
 constexpr int kLfFused = 0, kLfH = 1, kLfE = 2;
 
 template <typename T, bool UNIT_D, int TJ, int MODE>
-__global__ void __launch_bounds__(ib::lf_max_threads(sizeof(T)), sizeof(T) == 8 ? 1 : 2)
+__global__ void __launch_bounds__(ib::lf_max_threads(sizeof(T)), 1)
     k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int x0, int npl, int tiles,
               int chunks, int nstages, T c_h, T c_e, T d, T *halo_h, int64_t fs_h, T *halo_e,
               int64_t fs_e) {

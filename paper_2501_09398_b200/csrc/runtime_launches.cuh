@@ -169,7 +169,17 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
         const int64_t slots = (int64_t)std::max(1, per_sm) * c->num_sms;
         int64_t rpc = env_int("IB_HOTSPOT_RPC", 0);
-        if (rpc <= 0) rpc = std::max<int64_t>(16, std::min<int64_t>(128, (int64_t)rows * tiles / (12 * slots)));
+        if (rpc <= 0) {
+          rpc = std::max<int64_t>(16, std::min<int64_t>(128, (int64_t)rows * tiles / (12 * slots)));
+          // Few waves: a partial last wave idles most SMs for a whole CTA's march (Hotspot2D 4096^2:
+          // 512 CTAs on 444 slots), so round the grid to whole waves (>= 8 rows per CTA).
+          const int64_t ctas = tiles * ((rows + rpc - 1) / rpc);
+          if (ctas < 3 * slots) {
+            const int64_t waves = std::max<int64_t>(1, (ctas + slots / 2) / slots);
+            const int64_t chunks = std::max<int64_t>(1, waves * slots / tiles);
+            rpc = std::max<int64_t>(8, (rows + chunks - 1) / chunks);
+          }
+        }
         rpc = std::min<int64_t>(rpc, rows);
         dim3 grid((unsigned)tiles, (unsigned)((rows + rpc - 1) / rpc));
         Launch Lz = make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, (int)rpc, ns,
@@ -275,6 +285,8 @@ Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int
   if (chunks <= 0) chunks = std::max<int64_t>(1, slots / tiles);
   chunks = std::min<int64_t>(chunks, npl);  // every chunk non-empty
   int64_t ctas = env_int("IB_FDTD_CTAS", 0);
+  if (ctas <= 0 && env_int("IB_FDTD_CHUNKS", 0) <= 0 && tiles > slots) ctas = slots;  // > one wave of
+  // tiles (long rows force short tiles, e.g. 384^3): one wave, the unit list split evenly
   if (ctas <= 0) {
     ctas = tiles * chunks;  // one CTA per (tile, chunk): the kernel maps blockIdx.x to both
   } else {
@@ -373,16 +385,18 @@ void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
       // 128 / 256 / 512 / 1024); IB_VECTOR_BLOCK overrides
       int64_t bs = env_int("IB_VECTOR_BLOCK", 128);
       bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
+      // grid: one work item per thread, capped at 8 waves of resident threads (grid-stride beyond)
+      const int64_t cap_ctas = 8LL * c->num_sms * (2048 / bs);
       if (c->dtype == IB_F32) {
-        const int64_t threads = (n >> 2) + (n & 3);
-        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
-        out.push_back(make_launch((const void *)ib::k_vector_f32, grid, block, 0,
-                                  (float *)c->field[0], n, cc));
+        const int64_t threads = (n >> 2) + (n & 3), need = (threads + bs - 1) / bs;
+        dim3 block((unsigned)bs), grid((unsigned)std::min<int64_t>(cap_ctas, need));
+        const void *fn = need > cap_ctas ? (const void *)ib::k_vector_f32<true> : (const void *)ib::k_vector_f32<false>;
+        out.push_back(make_launch(fn, grid, block, 0, (float *)c->field[0], n, cc));
       } else {
-        const int64_t threads = (n >> 1) + (n & 1);
-        dim3 block((unsigned)bs), grid((unsigned)((threads + bs - 1) / bs));
-        out.push_back(make_launch((const void *)ib::k_vector_f64, grid, block, 0,
-                                  (double *)c->field[0], n, cc));
+        const int64_t threads = (n >> 1) + (n & 1), need = (threads + bs - 1) / bs;
+        dim3 block((unsigned)bs), grid((unsigned)std::min<int64_t>(cap_ctas, need));
+        const void *fn = need > cap_ctas ? (const void *)ib::k_vector_f64<true> : (const void *)ib::k_vector_f64<false>;
+        out.push_back(make_launch(fn, grid, block, 0, (double *)c->field[0], n, cc));
       }
       break;
     }
