@@ -381,12 +381,15 @@ void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     case IB_SOLVER_VECTOR: {
       const int64_t n = c->dims[0];
       const double cc = c->scalars[0];
-      // 128-thread CTAs measured best (1.21 / 1.23 / 1.24 / 1.40 us per iteration in a PDL graph at
-      // 128 / 256 / 512 / 1024); IB_VECTOR_BLOCK overrides
-      int64_t bs = env_int("IB_VECTOR_BLOCK", 128);
+      // Small vectors (the skeleton, 2^14): one item per thread in 128-thread CTAs (measured best:
+      // 1.21 / 1.23 / 1.24 / 1.40 us per iteration at 128 / 256 / 512 / 1024). Beyond one wave of
+      // threads CTA dispatch dominates (~1.2 ns per CTA: 8192 CTAs for 2^22 elements), so
+      // 1024-thread CTAs, two per SM, grid-stride. IB_VECTOR_BLOCK overrides the block size.
+      const int64_t items = c->dtype == IB_F32 ? (n >> 2) + (n & 3) : (n >> 1) + (n & 1);
+      const bool big = items > 2048LL * c->num_sms;
+      int64_t bs = env_int("IB_VECTOR_BLOCK", big ? 1024 : 128);
       bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
-      // grid: one work item per thread, capped at 8 waves of resident threads (grid-stride beyond)
-      const int64_t cap_ctas = 8LL * c->num_sms * (2048 / bs);
+      const int64_t cap_ctas = big ? 2LL * c->num_sms * (2048 / bs) / 2 : 8LL * c->num_sms * (2048 / bs);
       if (c->dtype == IB_F32) {
         const int64_t threads = (n >> 2) + (n & 3), need = (threads + bs - 1) / bs;
         dim3 block((unsigned)bs), grid((unsigned)std::min<int64_t>(cap_ctas, need));

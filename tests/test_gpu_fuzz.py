@@ -75,3 +75,16 @@ def test_fuzz_vector(gpu, dtype):
         got = wl.run_batched(wl.vector_program(), st, kk, nb, dtype=dtype, pdl=bool(rng.integers(2))).values
         assert np.array_equal(np.asarray(got, npd), want), (c, n, cst, kk, nb)
     wl.release_cached_contexts()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_large_vector_grid_stride(gpu, dtype):
+    """Vectors beyond one wave of threads take 1024-thread CTAs and a grid-stride loop."""
+    npd = np.float32 if dtype == "f32" else np.float64
+    rng = np.random.default_rng(7)
+    for n in (5_000_003, 3 * 1024 * 1024 * 4 + 2):
+        st = wl.VectorWorkload(rng.random(n), 0.9999)
+        want = ocpu.vector(st.values, 0.9999, 6, npd)
+        got = wl.run_batched(wl.vector_program(), st, 3, 2, dtype=dtype, pdl=True).values
+        assert np.array_equal(np.asarray(got, npd), want), n
+    wl.release_cached_contexts()
