@@ -306,8 +306,13 @@ Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int
 // staged kernel's CTA (or IB_FDTD_KERNEL=lean).
 template <typename T>
 void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
+  // The staged kernel marches planes serially per CTA; while the lattice sits in L2 the fully
+  // parallel lean kernels finish sooner (measured us/iter, staged vs lean: 32^3 6.8 / 5.1, 64^3
+  // 8.3 / 7.8, 96^3 17.3 / 15.1, 128^3 28.0 / 28.2, 160^3 66.7 / 71.5). IB_FDTD_KERNEL=lean|staged.
   const char *force = env_str("IB_FDTD_KERNEL");
-  const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0;
+  const int64_t lattice_bytes = 6 * c->lat_fs * c->esize;
+  const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0 ||
+                    (!force && c->slabs.size() == 1 && !c->dist() && lattice_bytes < (40LL << 20));
   const int nx = (int)c->dims[0];
   const int P = (int)c->slabs.size();
   if (c->dist()) {  // one rank's slab; the neighbours' halo planes through IPC mappings
