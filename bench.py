@@ -301,6 +301,7 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
             },
             "k_sweep": sweep,
             "clocks": clocks.summary(),
+            "launches": solver.describe(),  # the kernels one iteration ran (ib_describe)
         }
         if headline:
             out["e2e"] = measure_e2e(solver, state, k, num, n, pdl, args)

@@ -122,6 +122,10 @@ int ib_upload(ib_ctx *ctx, int field, const void *host, size_t bytes);
 int ib_download(ib_ctx *ctx, int field, void *host, size_t bytes);
 /* Bytes one iteration moves by the roofline convention (every array read once, written once). */
 int64_t ib_iteration_bytes(const ib_ctx *ctx);
+/* The kernels one iteration launches (the variant the runtime chose for this shape and device):
+ * a JSON array of {"kernel", "grid", "block", "smem", "slab", "step"}, NUL-terminated into buf
+ * (truncated to cap). Returns the full length including the NUL, or a negative status. */
+int64_t ib_describe(ib_ctx *ctx, char *buf, int64_t cap);
 
 /* ---- stream mode: run_loop (Listing 1) ------------------------------------------------------- */
 int ib_run_stream(ib_ctx *ctx, int64_t iterations, int flags, ib_times *times);

@@ -405,6 +405,37 @@ int64_t ib_field_bytes(const ib_ctx *c, int field) {
   return numel(c->fshape[field], c->fndim[field]) * c->esize;
 }
 
+int64_t ib_describe(ib_ctx *c, char *buf, int64_t cap) {
+  IB_TRY(check_ctx(c));
+  DeviceGuard guard;
+  IB_CUDA(cudaSetDevice(c->slabs[0].device));
+  std::vector<Launch> v;
+  iteration_launches(c, c->cur, v);
+  std::string js = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    const Launch &L = v[i];
+    const char *name = nullptr;
+    if (cudaFuncGetName(&name, L.func) != cudaSuccess || !name) {
+      cudaGetLastError();
+      name = "?";
+    }
+    char row[640];
+    std::snprintf(row, sizeof(row),
+                  "%s{\"kernel\": \"%s\", \"grid\": [%u, %u, %u], \"block\": [%u, %u, %u], "
+                  "\"smem\": %zu, \"slab\": %d, \"step\": %d}",
+                  i ? ", " : "", name, L.grid.x, L.grid.y, L.grid.z, L.block.x, L.block.y, L.block.z,
+                  L.smem, L.slab, L.step);
+    js += row;
+  }
+  js += "]";
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>((size_t)cap - 1, js.size());
+    std::memcpy(buf, js.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)js.size() + 1;
+}
+
 int64_t ib_iteration_bytes(const ib_ctx *c) {
   if (!c) return -1;
   const int64_t es = c->esize;

@@ -494,6 +494,19 @@ class DeviceSolver:
     def flush_l2(self) -> None:
         _lib.check(_lib.lib().ib_flush_l2(self.ctx))
 
+    def describe(self) -> list:
+        """The kernel launches of one iteration as the runtime chose them for this shape:
+        [{"kernel", "grid", "block", "smem", "slab", "step"}, ...] (ib_describe)."""
+        import json
+
+        L = _lib.lib()
+        n = int(L.ib_describe(self.ctx, None, 0))
+        if n < 0:
+            _lib.check(n)
+        buf = ctypes.create_string_buffer(n)
+        L.ib_describe(self.ctx, buf, n)
+        return json.loads(buf.value.decode())
+
     @property
     def iteration_bytes(self) -> int:
         return int(_lib.lib().ib_iteration_bytes(self.ctx))

@@ -313,3 +313,27 @@ def test_plain_c_caller_runs_and_matches_python(gpu, tmp_path):
     st = wl.HotspotWorkload(t.reshape(n, n).astype(np.float64), p.reshape(n, n).astype(np.float64), 0.1)
     got = wl.run_batched(wl.hotspot_program(), st, 20, 10, dtype="f32", pdl=True).temperature
     assert abs(float(got[0, 0]) - t0) <= 1e-6 * max(1.0, abs(t0))
+
+
+def test_describe_reports_the_chosen_variants(gpu):
+    """ib_describe: the launch list the runtime picked for the BASELINE shapes."""
+    def kernels(workload, size, **kw):
+        s = wl.DeviceSolver(cli.build_workload(workload, size), "f32", **kw)
+        try:
+            return s.describe()
+        finally:
+            s.close()
+
+    (h2,) = kernels("hotspot2d", [1024])
+    assert h2["kernel"].startswith("_ZN2ib13k_hotspot_vec") and h2["block"] == [256, 2, 1]
+    (h3,) = kernels("hotspot3d", [512, 8])
+    assert h3["kernel"].startswith("_ZN2ib13k_hotspot_vec") and h3["block"] == [256, 1, 1]
+    f = kernels("fdtd", [256])
+    assert len(f) == 2 and all("k_fdtd_lf" in k["kernel"] for k in f) and [k["step"] for k in f] == [0, 1]
+    assert all(k["smem"] > 200 * 1024 for k in f)  # the 6-stage ring
+    (ff,) = kernels("fdtd", [256], fuse=True)
+    assert "k_fdtd_lf" in ff["kernel"]
+    small = kernels("fdtd", [32])
+    assert [("k_fdtd_h2" in k["kernel"], "k_fdtd_e2" in k["kernel"]) for k in small] == [(True, False), (False, True)]
+    (v,) = kernels("vector", [16384])
+    assert "k_vector_f32" in v["kernel"] and v["grid"] == [32, 1, 1]
