@@ -11,7 +11,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libiterbatch_b200.so")
+LIB_PATH = os.environ.get("IB_LIB_PATH") or os.path.join(PKG, "libiterbatch_b200.so")  # override: A/B tooling
 
 IB_OK, IB_EINVAL, IB_ECUDA, IB_ENOMEM, IB_ESTATE, IB_ENODEV = 0, -1, -2, -3, -4, -5
 SOLVER = {"vector": 0, "hotspot2d": 1, "hotspot3d": 2, "fdtd": 3, "fdtd_fused": 4}

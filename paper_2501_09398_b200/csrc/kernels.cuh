@@ -599,8 +599,11 @@ __global__ void __launch_bounds__(256)
 // (TJ = 6 / 8 with one CTA per SM measured no faster than TJ = 4: 141.6 / 212.9 vs 142.6 us fused.)
 // binary64 rows hold half as many elements per 16-byte group, so a tile row needs twice the
 // threads: up to 704 (4-row tiles, one CTA per SM).
-constexpr int kLfMaxThreads = 704;
-constexpr int lf_max_threads(int esize) { return esize == 8 ? 704 : kLfMaxThreads; }
+// WIDE instantiations take up to 704 threads (binary64 rows, long binary32 rows such as 384^3);
+// the narrow ones keep two CTAs per SM in the register file, which also schedules ~1-2% faster
+// at 256^3 binary32 (measured A/B: 133.1 vs 134.7 us fused, 193.3 vs 197.0 two half-steps).
+constexpr int kLfMaxThreads = 704, kLfNarrowThreads = 384;
+constexpr int lf_max_threads(int) { return kLfMaxThreads; }
 // MODE: kLfFused (above), kLfH / kLfE = the H or the E half-step alone, in place (src == dst),
 // the two-launch leapfrog of the reference's program (workloads.py:325-413). Same staging and
 // march; H alone skips the seed plane and the E phase, E alone loads H instead of computing it and
@@ -609,8 +612,8 @@ constexpr int lf_max_threads(int esize) { return esize == 8 ? 704 : kLfMaxThread
 // launch) or rows it never uses (H halo in the H launch, E halo in the E launch).
 constexpr int kLfFused = 0, kLfH = 1, kLfE = 2;
 
-template <typename T, bool UNIT_D, int TJ, int MODE>
-__global__ void __launch_bounds__(ib::lf_max_threads(sizeof(T)), 1)
+template <typename T, bool UNIT_D, int TJ, int MODE, bool WIDE>
+__global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThreads, WIDE ? 1 : 2)
     k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int x0, int npl, int tiles,
               int chunks, int nstages, T c_h, T c_e, T d, T *halo_h, int64_t fs_h, T *halo_e,
               int64_t fs_e) {

@@ -242,21 +242,23 @@ inline LfConfig lf_config(const ib_ctx *c) {
   return LfConfig{};
 }
 
-template <typename T, bool U, int M>
-const void *lf_fn_m(int tj) {
+template <typename T, bool U, int M, bool W>
+const void *lf_fn_w(int tj) {
   switch (tj) {
-    case 1: return (const void *)ib::k_fdtd_lf<T, U, 1, M>;
-    case 2: return (const void *)ib::k_fdtd_lf<T, U, 2, M>;
-    case 3: return (const void *)ib::k_fdtd_lf<T, U, 3, M>;
-    default: return (const void *)ib::k_fdtd_lf<T, U, 4, M>;
+    case 1: return (const void *)ib::k_fdtd_lf<T, U, 1, M, W>;
+    case 2: return (const void *)ib::k_fdtd_lf<T, U, 2, M, W>;
+    case 3: return (const void *)ib::k_fdtd_lf<T, U, 3, M, W>;
+    default: return (const void *)ib::k_fdtd_lf<T, U, 4, M, W>;
   }
 }
+template <typename T, bool U, int M>
+const void *lf_fn_m(int tj, bool wide) { return wide ? lf_fn_w<T, U, M, true>(tj) : lf_fn_w<T, U, M, false>(tj); }
 template <typename T>
-const void *lf_fn(bool unit, int tj, int mode) {
-  if (unit) return mode == ib::kLfH ? lf_fn_m<T, true, ib::kLfH>(tj)
-                   : mode == ib::kLfE ? lf_fn_m<T, true, ib::kLfE>(tj) : lf_fn_m<T, true, ib::kLfFused>(tj);
-  return mode == ib::kLfH ? lf_fn_m<T, false, ib::kLfH>(tj)
-         : mode == ib::kLfE ? lf_fn_m<T, false, ib::kLfE>(tj) : lf_fn_m<T, false, ib::kLfFused>(tj);
+const void *lf_fn(bool unit, int tj, int mode, bool wide) {
+  if (unit) return mode == ib::kLfH ? lf_fn_m<T, true, ib::kLfH>(tj, wide)
+                   : mode == ib::kLfE ? lf_fn_m<T, true, ib::kLfE>(tj, wide) : lf_fn_m<T, true, ib::kLfFused>(tj, wide);
+  return mode == ib::kLfH ? lf_fn_m<T, false, ib::kLfH>(tj, wide)
+         : mode == ib::kLfE ? lf_fn_m<T, false, ib::kLfE>(tj, wide) : lf_fn_m<T, false, ib::kLfFused>(tj, wide);
 }
 
 // One k_fdtd_lf launch of `mode` from lattice buffer `from` to `to` (equal for the in-place
@@ -268,9 +270,9 @@ Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int
   const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
   const bool unit = c->scalars[0] == 1.0;
   const LfConfig cfg = lf_config(c);
-  const void *fn = lf_fn<T>(unit, cfg.tj, mode);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
   const int threads = lf_threads(c, cfg.tj);
+  const void *fn = lf_fn<T>(unit, cfg.tj, mode, threads > ib::kLfNarrowThreads);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, cfg.smem);
   // Lockstep (tile, x-chunk) grid: as many x-chunks as the resident slots hold whole columns of
