@@ -32,6 +32,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -286,6 +287,10 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
             "stream_us_per_iter": 1e6 * stream_mean / n,
             "stream_pdl_us_per_iter": 1e6 * statistics.fmean(stream_pdl) / n,
             "speedup_vs_stream": stream_mean / step_mean,
+            # the reference's error model (model.py:247-253): relative std errors in quadrature
+            "speedup_vs_stream_err": (stream_mean / step_mean) * math.hypot(
+                statistics.stdev(stream_s) / stream_mean if len(stream_s) > 1 else 0.0,
+                statistics.stdev(step_s) / statistics.fmean(step_s) if len(step_s) > 1 else 0.0),
             "speedup_vs_stream_exec_only": stream_mean / exec_mean,
             "kernels_per_iter": kpi,
             "gpu_launches": args.steps * n * kpi,
@@ -600,6 +605,7 @@ def run_ours(args, dist: Dist) -> int:
                   "stays L2-resident across the run's iterations as in the real application",
         },
         "speedup_vs_stream": round(head["speedup_vs_stream"], 3),
+        "speedup_vs_stream_err": round(head["speedup_vs_stream_err"], 4),
         "stream_us_per_iter": round(head["stream_us_per_iter"], 4),
         "stream_pdl_us_per_iter": round(head["stream_pdl_us_per_iter"], 4),
         "graph_exec_us_per_iter": round(head["graph_exec_us_per_iter"], 4),
