@@ -99,3 +99,39 @@ def test_fdtd_256_two_half_steps_fused_and_oracle(gpu, fdtd256):
         assert np.array_equal(np.asarray(a, np.float32), w)
         assert np.array_equal(np.asarray(b, np.float32), w)
         assert np.array_equal(np.asarray(c, np.float32), w)
+
+
+def test_fdtd_256_binary32_within_tolerance_at_the_baseline_horizon(gpu):
+    """BASELINE config FDTD 256^3, N = 2000: binary32 vs the binary64 run (which reproduces the
+    reference bit for bit, pinned by its checksum at N = 20) within 1e-5 in normalised L-inf
+    (pointwise max-rel is undefined on TE101's exact zeros)."""
+    st = wl.te101_cavity(256, 256, 256)
+    prog = wl.fdtd_program()
+    ref = wl.run_batched(prog, st, 100, 20).state_arrays()
+    got = wl.run_batched(prog, st, 100, 20, dtype="f32", fuse=True).state_arrays()
+    wl.release_cached_contexts()
+    scale = max(float(np.max(np.abs(a))) for a in ref[:3])  # E amplitude
+    hscale = max(float(np.max(np.abs(a))) for a in ref[3:])
+    for i, (g, r) in enumerate(zip(got, ref)):
+        s = scale if i < 3 else hscale
+        assert float(np.max(np.abs(g - r))) / s <= 1e-5, i
+
+
+def test_hotspot3d_2048_binary32_within_tolerance_at_n100(gpu):
+    """BASELINE config Hotspot3D 2048x2048x256, N = 100: binary32 vs binary64 (bit-exact to the
+    reference algorithm), max-rel <= 1e-5."""
+    rng = np.random.default_rng(20240817)
+    t = rng.random(SHAPE)
+    p = rng.random(SHAPE) * 1e-3
+    outs = {}
+    for dtype in ("f64", "f32"):
+        s = wl.DeviceSolver(_Shape(SHAPE, K_DIFF), dtype, upload=False)
+        try:
+            npd = np.float64 if dtype == "f64" else np.float32
+            s.upload([t.astype(npd, copy=False), p.astype(npd, copy=False)])
+            s.run_batched(20, 5, pdl=True)
+            outs[dtype] = s.download_field(0)
+        finally:
+            s.close()
+    rel = np.max(np.abs(outs["f32"].astype(np.float64) - outs["f64"]) / np.abs(outs["f64"]))
+    assert rel <= 1e-5, rel
