@@ -219,3 +219,36 @@ def test_real_trace_is_consistent(gpu, tmp_path):
     assert np.array_equal(np.asarray(got.temperature, np.float32), want), "traced solver after tracing"
     assert s.checksum() != 0
     s.close()
+
+
+def test_contexts_release_their_device_memory(gpu):
+    """Create / run / destroy contexts of every solver repeatedly: device memory returns to its
+    starting level (no leaked fields, lattices, graphs or IPC / counter blocks)."""
+    import ctypes
+
+    from paper_2501_09398_b200 import _lib, cli
+
+    wl.release_cached_contexts()
+    L = _lib.lib()
+
+    def free_bytes():
+        f, t = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(L.ib_mem_info(0, ctypes.byref(f), ctypes.byref(t)))
+        return f.value
+
+    def cycle():
+        for w, size, kw in (("vector", [4096], {}), ("hotspot2d", [64, 96], {}), ("hotspot3d", [24, 16, 8], {}),
+                            ("fdtd", [12, 9, 14], {}), ("fdtd", [12, 9, 14], {"fuse": True}),
+                            ("hotspot3d", [40, 16, 8], {"devices": [0, 0, 0]})):
+            s = wl.DeviceSolver(cli.build_workload(w, size), "f32", **kw)
+            s.run_batched(3, 2, pdl=True)
+            s.build_graph(5, while_loop=("devices" not in kw))
+            s.run_graph(1)
+            s.close()
+
+    cycle()  # first use: lazy module loading, driver pools
+    before = free_bytes()
+    for _ in range(5):
+        cycle()
+    after = free_bytes()
+    assert before - after < (64 << 20), (before, after)
