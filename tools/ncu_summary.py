@@ -46,8 +46,12 @@ UNIT = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s
 
 
 def raw(rep: str) -> list[dict]:
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
-                         capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):  # `ncu --page raw --csv` already exported on the GPU box
+        with open(rep) as fh:
+            out = fh.read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -86,7 +90,9 @@ def main():
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = {}
     for rep, key in REPORTS.items():
-        path = os.path.join(a.dir, f"ncu_{rep}.ncu-rep")
+        path = os.path.join(a.dir, f"ncu_{rep}_raw.csv")
+        if not os.path.exists(path):
+            path = os.path.join(a.dir, f"ncu_{rep}.ncu-rep")
         if not os.path.exists(path):
             continue
         per_kernel = {}

@@ -1,6 +1,7 @@
 #!/bin/bash
 # ncu evidence for the committed kernels (run under gpurun; one GPU; never multi-rank).
-# Writes gpurun_out/ncu_<name>.ncu-rep (--set full) and gpurun_out/launches_bench.csv.
+# Writes gpurun_out/ncu_<name>_raw.csv (every metric of the --set full capture; the .ncu-rep is
+# kept only with KEEP_REPS=1) and gpurun_out/launches_bench.csv.
 set -u
 cd "${GRAFT_REPO_ROOT:-.}"
 full() {  # name regex skip -- profile_run.py args
@@ -8,6 +9,10 @@ full() {  # name regex skip -- profile_run.py args
   timeout 300 ncu --set full --clock-control none --import-source on -k "regex:$rx" -s "$skip" -c 2 \
     -o "gpurun_out/ncu_$name" python tools/profile_run.py "$@" > "gpurun_out/ncu_$name.log" 2>&1
   echo "ncu full $name rc=$?"
+  # keep gpurun_out small enough to come back (64 MiB): every raw metric as CSV, the report only
+  # with KEEP_REPS=1
+  ncu -i "gpurun_out/ncu_$name.ncu-rep" --page raw --csv > "gpurun_out/ncu_${name}_raw.csv" 2>/dev/null
+  [ "${KEEP_REPS:-0}" = 1 ] || rm -f "gpurun_out/ncu_$name.ncu-rep"
 }
 full hotspot2d k_hotspot 2 --workload hotspot2d --size 1024 --iters 4
 full hotspot3d_512 k_hotspot 2 --workload hotspot3d --size 512,8 --iters 4
