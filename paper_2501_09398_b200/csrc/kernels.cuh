@@ -180,12 +180,17 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // T is (R+2)/R of the grid instead of 3x). Every edge clamp (np.pad "edge", workloads.py:177) is
 // an address clamp computed once per thread — the clamped neighbour of an edge cell is the cell
 // itself — so the per-row work is 5 loads, 1 store and the cell arithmetic, with 32-bit offsets
-// (the launch layer checks the slab buffer holds < 2^31 elements).
+// (the launch layer checks the slab buffer holds < 2^31 elements). SH = 1: when a warp covers 32
+// groups of one row and whole y-rows, the in-row (2-D) / z (3-D) neighbours come from the
+// adjacent lanes by shuffles and only the warp's edge lanes load (SH = 2 also shuffles the y
+// rows — measured slower). The power field, never written by a step, is loaded before the PDL
+// wait.
 // Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles a
-// y-row). block = (bx groups of a row, by row-blocks), 256 threads by default: an EMPTY kernel's
-// per-launch floor in a PDL graph falls with fewer, bigger CTAs (1024 x 256 threads 1.41 us,
-// 256 x 1024 0.57 us, tools/microbench_floor.cu), but this kernel measured slower with 512- and
-// 1024-thread CTAs — a CTA retires at its slowest warp. grid = (ceil(M/V/bx), ceil(rows/(R*by))).
+// y-row). block = (bx groups of a row, by row-blocks): 512 threads (256 x 2) for 2-D, 256 for
+// 3-D by default (launch layer). An EMPTY kernel's per-launch floor in a PDL graph falls with
+// fewer, bigger CTAs (1024 x 256 threads 1.41 us, 256 x 1024 0.57 us, tools/microbench_floor.cu),
+// but 1024-thread CTAs measured slower here — a CTA retires at its slowest warp.
+// grid = (ceil(M/V/bx), ceil(rows/(R*by))).
 // Measured alternatives that were not faster in-graph (Hotspot2D 1024^2 / Hotspot3D 512^2x8):
 // 2-D CTAs sharing x rows through L1, 2-4 warp-strided groups per thread (fewer instructions per
 // cell), a whole y-row per thread, a shared-memory tile staging the x rows once per CTA (+40%:
