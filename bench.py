@@ -210,16 +210,20 @@ def pick_k(solver, cfg, quick: bool) -> tuple[int, bool, list]:
     cands = [k for k in cfg["k_candidates"] if n % k == 0]
     if quick:
         cands = [k for k in cands if k in (10, 100, 1000)] or cands[:2]
-    rows = []
+    reps = 1 if quick else 3  # median of 3: one host hiccup inside a graph build (T_C) would
+    rows = []                 # otherwise mark a K as slow
     best = None
     for k in cands:
         for pdl in (False, True):
-            solver.flush_l2()
-            t = solver.run_batched(k, n // k, pdl=pdl)
-            rows.append({"K": k, "pdl": pdl, "us_per_iter": 1e6 * t.gpu_s / n,
-                         "T_C_us": 1e6 * t.build_s})
-            if best is None or t.gpu_s < best[0]:
-                best = (t.gpu_s, k, pdl)
+            ts = []
+            for _ in range(reps):
+                solver.flush_l2()
+                ts.append(solver.run_batched(k, n // k, pdl=pdl))
+            g = statistics.median(t.gpu_s for t in ts)
+            rows.append({"K": k, "pdl": pdl, "us_per_iter": 1e6 * g / n,
+                         "T_C_us": 1e6 * statistics.median(t.build_s for t in ts), "samples": reps})
+            if best is None or g < best[0]:
+                best = (g, k, pdl)
     return best[1], best[2], rows
 
 

@@ -69,7 +69,7 @@ int main() {
     }
   }
   // empty-kernel floor vs grid shape (same thread count where possible)
-  const int shapes[][2] = {{1024, 256}, {512, 512}, {256, 1024}, {2048, 128}, {148, 1024}, {32, 128}, {1, 32}};
+  const int shapes[][2] = {{1024, 256}, {512, 512}, {256, 512}, {128, 1024}, {256, 1024}, {2048, 128}, {148, 1024}, {32, 128}, {1, 32}};
   for (auto sh : shapes) {
     cudaGraph_t g; cudaGraphExec_t ge;
     cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
