@@ -94,7 +94,8 @@ class Dist:
             if self.world > n:  # protocol check on a small box: ranks share GPUs, gloo for plumbing
                 self.shared = True
                 self.local = self.local % max(1, n)
-                torch.cuda.set_device(self.local)
+                if n:  # (none at all: the reference arm, CPU only)
+                    torch.cuda.set_device(self.local)
                 td.init_process_group("gloo")
             else:
                 torch.cuda.set_device(self.local)
