@@ -112,6 +112,16 @@ int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndim
               const double *scalars, int nscalars, const int *devices, int ndevices);
 void ib_destroy(ib_ctx *ctx);
 
+/* Halo exchange of a multi-slab hotspot context (ib_create with ndevices > 1), SURVEY.md §8e:
+ * IB_HALO_STORE (default, v2) — each slab's stencil kernel stores its boundary planes straight into
+ * the neighbours' halo planes; IB_HALO_COPY (v1) — the kernel writes only its own slab and one
+ * peer cudaMemcpyAsync (UVA) per face follows it on the slab's stream (memcpy nodes in the captured
+ * graph). Same results bit for bit. Drops any built graph. EINVAL for other solvers / contexts
+ * (FDTD slabs, ib_create_dist). Single-slab contexts accept either and ignore it. */
+#define IB_HALO_STORE 0
+#define IB_HALO_COPY 1
+int ib_set_halo_mode(ib_ctx *ctx, int mode);
+
 /* Fields, in the reference's state_arrays() order (workloads.py:93,163,272):
  * vector: 0 values ; hotspot: 0 temperature, 1 power ; fdtd: 0 ex 1 ey 2 ez 3 hx 4 hy 5 hz.
  * Host buffers are C-contiguous in the context dtype; bytes must equal the full field size. */

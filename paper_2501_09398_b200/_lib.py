@@ -84,6 +84,7 @@ PROTOTYPES = [
     ("ib_slab_info", _I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I),
                           ctypes.POINTER(_I)]),
     ("ib_describe", _I64, [_P, ctypes.c_char_p, _I64]),
+    ("ib_set_halo_mode", _I, [_P, _I]),
     ("ib_ipc_export", _I, [_P, _P, _SZ]),
     ("ib_ipc_attach", _I, [_P, _P, _P]),
     ("ib_trace_enable", _I, [_P, _I64]),

@@ -46,6 +46,9 @@ struct ib_ctx {
   int peer_rows_up = 0;  // the up neighbour's owned rows (locates its bottom halo plane)
   int peer_rows_dn = 0;  // the down neighbour's (FDTD: its lattice field stride)
   bool peer = false;
+  // single-process slabs: halo planes by cudaMemcpyPeerAsync after each kernel (IB_HALO_COPY)
+  // instead of the kernel's own stores into the neighbours' halos
+  bool halo_copy = false;
   bool dist() const { return nranks > 1; }
   int64_t lattice_pitch() const { return lat_pitch; }
   // tracing (CUPTI activity records; host events on the CUPTI timebase)

@@ -60,6 +60,28 @@ int launch_dist_signal(ib_ctx *c, cudaStream_t st) {
   return launch_one(L, st, false);
 }
 
+// IB_HALO_COPY: slab g's first / last owned plane of an iteration's output
+// buf[outpar] into the neighbours' halo planes, one peer copy per face on slab g's stream right
+// after its kernel: cudaMemcpyAsync over UVA (peer access is enabled between slab devices;
+// cudaMemcpyPeerAsync cannot be captured), a memcpy node in the graph. Slab buffers are (rows + 2) planes:
+// top halo, owned rows, bottom halo.
+int halo_copies(ib_ctx *c, int g, int outpar, cudaStream_t st) {
+  const int P = (int)c->slabs.size();
+  Slab &s = c->slabs[g];
+  const size_t pb = (size_t)c->plane() * c->esize;
+  const char *b = (const char *)s.buf[outpar];
+  if (g > 0) {
+    Slab &n = c->slabs[g - 1];
+    IB_CUDA(cudaMemcpyAsync((char *)n.buf[outpar] + (size_t)(n.rows() + 1) * pb, b + pb, pb, cudaMemcpyDefault, st));
+  }
+  if (g + 1 < P) {
+    Slab &n = c->slabs[g + 1];
+    IB_CUDA(cudaMemcpyAsync(n.buf[outpar], b + (size_t)s.rows() * pb, pb, cudaMemcpyDefault, st));
+  }
+  return IB_OK;
+}
+bool copies_halos(const ib_ctx *c) { return c->halo_copy && c->slabs.size() > 1 && c->hotspot(); }
+
 // Enqueue `iters` iterations starting at `parity` onto the slab streams (also used under stream
 // capture). Multi-slab: kernel(g,t) waits for kernel(g+-1,t-1) — RAW on the halo it reads and
 // WAR on the halo it writes — through double-buffered events.
@@ -96,6 +118,7 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
       c->ev(single_stream ? IB_EV_NODE_ADDED : IB_EV_BASELINE_KERNEL_LAUNCHED, single_stream ? -1 : t,
             single_stream ? nk : (int64_t)q);
       IB_TRY(launch_one(L, st, use_pdl));
+      if (copies_halos(c)) IB_TRY(halo_copies(c, L.slab, par ^ 1, st));
       if (P > 1) IB_CUDA(cudaEventRecord(s.ev[f & 1], st));
       if (c->peer) IB_TRY(launch_dist_signal(c, st));  // its halo planes went out with its stores
       ++nk;

@@ -100,11 +100,11 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     const T *src = (const T *)s.buf[parity] + off;
     T *dst = (T *)s.buf[parity ^ 1] + off;
     T *up = nullptr, *dn = nullptr;
-    if (P > 1 && g > 0) {  // my first owned row -> upper neighbour's bottom halo
+    if (P > 1 && g > 0 && !c->halo_copy) {  // my first owned row -> upper neighbour's bottom halo
       Slab &n = c->slabs[g - 1];
       up = (T *)n.buf[parity ^ 1] + (int64_t)(n.rows() + 1) * plane;
     }
-    if (P > 1 && g + 1 < P) {  // my last owned row -> lower neighbour's top halo
+    if (P > 1 && g + 1 < P && !c->halo_copy) {  // my last owned row -> lower neighbour's top halo
       Slab &n = c->slabs[g + 1];
       dn = (T *)n.buf[parity ^ 1];
     }

@@ -315,6 +315,9 @@ class Times:
         return cls(**t.as_dict())
 
 
+_HALO_MODE = {"store": 0, "copy": 1}  # IB_HALO_STORE / IB_HALO_COPY
+
+
 class DeviceSolver:
     """A solver instance resident in HBM: upload once, run many iterations, download once.
 
@@ -325,8 +328,12 @@ class DeviceSolver:
         instantiated/uploaded once and replayed.
     """
 
-    def __init__(self, state, dtype="f64", devices=None, upload: bool = True, fuse: bool = False):
+    def __init__(self, state, dtype="f64", devices=None, upload: bool = True, fuse: bool = False,
+                 halo: str = "store"):
         self.kind = _kind_of_state(state)
+        if halo not in _HALO_MODE:
+            raise ValueError(f"halo must be one of {sorted(_HALO_MODE)}, not {halo!r}")
+        self.halo = halo
         self.fused = bool(fuse)
         if self.fused and self.kind != "fdtd":
             raise ValueError("fuse=True applies to FDTD (H and E half-steps in one kernel)")
@@ -346,6 +353,8 @@ class DeviceSolver:
                         len(self.dims), sc, len(self.scalars), dv if devs else None, len(devs))
         )
         self._ctx = ctx
+        if halo != "store":  # multi-slab hotspot: peer-copy halo faces
+            _lib.check(L.ib_set_halo_mode(ctx, _HALO_MODE[halo]))
         self.nfields = L.ib_num_fields(ctx)
         self.shapes = []
         for f in range(self.nfields):

@@ -98,6 +98,46 @@ def test_hotspot_variants_with_slabs(gpu, env, kernel, slabs):
         assert np.array_equal(got.temperature, want), shape
 
 
+@pytest.mark.parametrize("kernel", ["vec", "tma", "scalar"])
+@pytest.mark.parametrize("slabs", [2, 3])
+def test_hotspot_slabs_copy_exchange(gpu, env, kernel, slabs):
+    """IB_HALO_COPY: the slab kernels write only their own rows and
+    cudaMemcpyPeerAsync moves the halo faces — == oracle in stream mode, per-step calls and
+    captured graphs at odd and even K, and equal to the fused-store exchange (v2)."""
+    env(IB_HOTSPOT_KERNEL=kernel, IB_HOTSPOT_RPC=3)
+    rng = np.random.default_rng(40 + slabs)
+    for shape in ((30, 12, 8), (41, 64)):
+        state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
+        want = ocpu.hotspot(state.temperature, state.power, 0.1, 6, np.float64)
+        with wl.DeviceSolver(state, "f64", devices=[0] * slabs, halo="copy") as s:
+            s.run_stream(6)
+            assert np.array_equal(s.download(state).temperature, want), shape
+            s.upload(state)
+            for _ in range(6):
+                s.run_step(0)
+            assert np.array_equal(s.download(state).temperature, want), shape
+            for k, n in ((3, 2), (2, 3), (6, 1)):
+                s.upload(state)
+                s.run_batched(k, n, build="capture", pdl=True)
+                assert np.array_equal(s.download(state).temperature, want), (shape, k)
+        with wl.DeviceSolver(state, "f32", devices=[0] * slabs, halo="copy") as s, \
+                wl.DeviceSolver(state, "f32", devices=[0] * slabs) as v2:
+            s.run_batched(3, 2, build="capture")
+            v2.run_batched(3, 2, build="capture")
+            assert np.array_equal(s.download(state).temperature, v2.download(state).temperature)
+
+
+def test_halo_mode_validation(gpu):
+    rng = np.random.default_rng(3)
+    hot = wl.HotspotWorkload(rng.random((8, 16)), rng.random((8, 16)) * 1e-3, 0.1)
+    with pytest.raises(ValueError):
+        wl.DeviceSolver(hot, "f32", halo="nvlink")
+    with wl.DeviceSolver(hot, "f32", halo="copy") as s:  # one slab: accepted, nothing to exchange
+        s.run_stream(2)
+    with pytest.raises(ValueError):
+        wl.DeviceSolver(wl.fdtd_cavity(6, 4, 6), "f32", devices=[0, 0], halo="copy")
+
+
 FDTD_DIMS = [(8, 4, 8), (5, 6, 7), (1, 1, 1), (3, 1, 9), (16, 9, 33), (2, 40, 3)]
 
 
