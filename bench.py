@@ -122,16 +122,61 @@ class Dist:
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------------------------
 class Clocks:
+    """SM clock and clock-event reasons sampled DURING a timed region: in-process NVML polling
+    every 50 ms (an nvidia-smi child polling the driver slowed graph instantiation inside the
+    region by milliseconds), nvidia-smi as the fallback. At least one sample is taken at the
+    region's end so short regions are covered."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.nvml = None
+        self.samples = []  # (sm_mhz, max_mhz, set of reasons)
         self.lines = []
+        self.start = 0
+        self._stop = threading.Event()
+        self.thread = None
+
+    def _nvml_index(self) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if ids and all(v.isdigit() for v in ids) and self.device < len(ids):
+            return int(ids[self.device])
+        return self.device
+
+    def _nvml_sample(self):
+        n = self.nvml
+        sm = n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self.handle, n.NVML_CLOCK_SM)
+        bits = n.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        flags = (n.nvmlClocksEventReasonHwSlowdown, n.nvmlClocksEventReasonHwThermalSlowdown,
+                 n.nvmlClocksEventReasonSwThermalSlowdown, n.nvmlClocksEventReasonSwPowerCap)
+        self.samples.append((float(sm), float(mx), {nm for nm, f in zip(self.NAMES, flags) if bits & f}))
+
+    def _nvml_loop(self):
+        while not self._stop.wait(0.05):
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
@@ -140,7 +185,7 @@ class Clocks:
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
             # nvidia-smi takes a few hundred ms to print its first line: wait for it so a short
-            # timed region (the skeleton's ~0.1 s) is still sampled; keep only later lines
+            # timed region is still sampled; keep only later lines
             t_end = time.monotonic() + 3.0
             while not self.lines and time.monotonic() < t_end and self.proc.poll() is None:
                 time.sleep(0.01)
@@ -154,6 +199,15 @@ class Clocks:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            try:
+                self._nvml_sample()  # the region's end
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
+            return
         if self.proc is not None:
             t_end = time.monotonic() + 0.3  # at least one sample from the region's end
             while len(self.lines) <= self.start and time.monotonic() < t_end and self.proc.poll() is None:
@@ -164,26 +218,24 @@ class Clocks:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
             self.thread.join(timeout=2)
+            for line in self.lines[self.start:]:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm, mx = float(parts[0]), float(parts[1])
+                except ValueError:
+                    continue
+                self.samples.append((sm, mx, {nm for nm, f in zip(self.NAMES, parts[3:7])
+                                              if f.lower() == "active"}))
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in self.lines[self.start:]:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for name, flag in zip(names, parts[3:7]):
-                if flag.lower() == "active":
-                    reasons.add(name)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = set().union(*(r for _, _, r in self.samples))
+        return {"sm_mhz": statistics.median(sm for sm, _, _ in self.samples),
+                "sm_max_mhz": self.samples[-1][1], "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def measured_peaks() -> tuple[float, str]:
