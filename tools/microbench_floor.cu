@@ -32,6 +32,14 @@ __global__ void k_rows(const float4 *a, float4 *b, const float4 *p, int n) {
   b[i] = make_float4(x.x + c.x + y.x + q.x, x.y + c.y + y.y + q.y, x.z + c.z + y.z + q.z, x.w + c.w + y.w + q.w);
 }
 
+__global__ void k_scale(const float4 *a, float4 *b, const float4 *, int n) {
+  pdl();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  float4 v = a[i];
+  const double c = 0.9999;
+  b[i] = make_float4((float)(v.x * c), (float)(v.y * c), (float)(v.z * c), (float)(v.w * c));
+}
+
 int main() {
   const int n = 1024 * 1024 / 4, K = 100, reps = 20;
   float4 *a, *b, *p;
@@ -94,6 +102,37 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("empty grid %5d x %4d    pdl=1  %.3f us/launch\n", sh[0], sh[1], 1000.f * ms / (reps * K));
     cudaGraphExecDestroy(ge); cudaGraphDestroy(g);
+  }
+  // the skeleton's shape: 2^14 floats, 32 x 128 threads, one float4 each, in place
+  {
+    const int ns = 4096;
+    const char *sn[4] = {"small empty", "small read", "small copy in place", "small scale (f64 mul) in place"};
+    void (*sf[4])(const float4 *, float4 *, const float4 *, int) = {k_empty, k_read, k_copy, k_scale};
+    for (int f = 0; f < 4; ++f) {
+      cudaGraph_t g; cudaGraphExec_t ge;
+      cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+      for (int k = 0; k < K; ++k) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ns / 128); cfg.blockDim = dim3(128); cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at; cfg.numAttrs = k > 0 ? 1 : 0;
+        cudaLaunchKernelEx(&cfg, sf[f], (const float4 *)a, a, (const float4 *)p, ns);
+      }
+      cudaStreamEndCapture(s, &g);
+      cudaGraphInstantiate(&ge, g, 0);
+      cudaGraphUpload(ge, s);
+      cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+      cudaGraphLaunch(ge, s);
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("%-32s pdl=1  %.3f us/launch\n", sn[f], 1000.f * ms / (reps * K));
+      cudaGraphExecDestroy(ge); cudaGraphDestroy(g);
+    }
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
