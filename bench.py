@@ -123,9 +123,10 @@ class Dist:
 # ---------------------------------------------------------------------------------------------
 class Clocks:
     """SM clock and clock-event reasons sampled DURING a timed region: in-process NVML polling
-    every 50 ms (an nvidia-smi child polling the driver slowed graph instantiation inside the
-    region by milliseconds), nvidia-smi as the fallback. At least one sample is taken at the
-    region's end so short regions are covered."""
+    every 200 ms (an nvidia-smi child polling the driver slowed graph instantiation inside the
+    region by milliseconds; each NVML query can still delay a concurrent build by ~0.1 ms, so
+    sparse), nvidia-smi as the fallback. One more sample is taken at the region's end so short
+    regions are covered."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -159,7 +160,7 @@ class Clocks:
         self.samples.append((float(sm), float(mx), {nm for nm, f in zip(self.NAMES, flags) if bits & f}))
 
     def _nvml_loop(self):
-        while not self._stop.wait(0.05):
+        while not self._stop.wait(0.2):
             try:
                 self._nvml_sample()
             except Exception:
