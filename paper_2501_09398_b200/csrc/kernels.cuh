@@ -35,6 +35,20 @@ template <> struct rn<double> {
 // its memory is visible. launch_dependents: allow the downstream grid to be scheduled now.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+// Cross-process peer exchange only (fence_sys, set for ib_ipc_attach'ed contexts): after halo
+// stores into a neighbour rank's buffer (CUDA IPC mapping, NVLink), the warp's stores are
+// performed at system scope before its threads retire, so the ordering flag a later kernel
+// publishes (k_dist_signal, release.sys) cannot overtake them in the fabric. One fence per warp:
+// __syncwarp orders the lanes' stores before the elected lane's fence.sc.sys, which is cumulative
+// over them. Costs ~4-7 us per iteration (the fence's system round trip), so single-process slabs,
+// ordered by CUDA's own cross-device graph edges, skip it.
+__device__ __forceinline__ void peer_fence() {
+  const unsigned am = __activemask();
+  unsigned lane;
+  asm("mov.u32 %0, %%laneid;" : "=r"(lane));
+  __syncwarp(am);
+  if (lane == (unsigned)(__ffs(am) - 1)) __threadfence_system();
+}
 
 // ================================================================================================
 // Skeleton: vector scale, in place.  workloads.py:97-105  out = values * c
@@ -107,13 +121,14 @@ template <typename T, bool D3>
 __global__ void __launch_bounds__(256)
     k_hotspot(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
               int rows, int C, int L, int rows_per_chunk, T k, T loss, int has_top, int has_bot,
-              T *__restrict__ halo_up, T *__restrict__ halo_dn) {
+              T *__restrict__ halo_up, T *__restrict__ halo_dn, int fence_sys) {
   pdl_trigger();
   const int64_t plane = (int64_t)C * L;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i0 = blockIdx.y * rows_per_chunk;
   const int i1 = min(rows, i0 + rows_per_chunk);
   pdl_wait();
+  bool halo_stored = false;  // stored into a neighbour's halo plane: fence before retiring
   if (p >= plane || i0 >= rows) return;
   const int j = D3 ? (int)(p / L) : (int)p;
   const int l = D3 ? (int)(p - (int64_t)j * L) : 0;
@@ -136,11 +151,18 @@ __global__ void __launch_bounds__(256)
     const T r = rn<T>::add(cur, rn<T>::mul(k, q));
     const T out = rn<T>::add(r, power[o + p]);
     dst[o + p] = out;
-    if (i == 0 && halo_up) halo_up[p] = out;
-    if (i == rows - 1 && halo_dn) halo_dn[p] = out;
+    if (i == 0 && halo_up) {
+      halo_up[p] = out;
+      halo_stored = true;
+    }
+    if (i == rows - 1 && halo_dn) {
+      halo_dn[p] = out;
+      halo_stored = true;
+    }
     up = cur;
     cur = dn;
   }
+  if (fence_sys && halo_stored) peer_fence();
 }
 
 // ---- vector helpers -------------------------------------------------------------------------
@@ -200,7 +222,7 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // the barrier serialises the load and compute rounds): the one-wave kernel is bound by its
 // memory round trip, and fewer, fatter or synchronised threads expose more latency.
 // ================================================================================================
-template <typename T, bool D3, int R, int SH = 0>
+template <typename T, bool D3, int R, int SH = 0, bool FS = false>
 __global__ void __launch_bounds__(1024)
     k_hotspot_vec(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
                   int rows, int C, int L, T k, T loss, int has_top, int has_bot,
@@ -299,8 +321,14 @@ __global__ void __launch_bounds__(1024)
       }
     }
     st16<T>(dst + i * M + m, out);
-    if (i == 0 && halo_up) st16<T>(halo_up + m, out);
-    if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
+    if (i == 0 && halo_up) {
+      st16<T>(halo_up + m, out);
+      if (FS) peer_fence();  // cross-process peer exchange only (template: no cost otherwise)
+    }
+    if (i == rows - 1 && halo_dn) {
+      st16<T>(halo_dn + m, out);
+      if (FS) peer_fence();  // cross-process peer exchange only (template: no cost otherwise)
+    }
   }
 }
 
@@ -351,7 +379,7 @@ template <typename T, bool D3, int G>
 __global__ void __launch_bounds__(256)
     k_hotspot_tma(const T *__restrict__ src, T *__restrict__ dst, const T *__restrict__ power,
                   int rows, int C, int L, int rows_per_cta, int nstages, T k, T loss, int has_top,
-                  int has_bot, T *__restrict__ halo_up, T *__restrict__ halo_dn) {
+                  int has_bot, T *__restrict__ halo_up, T *__restrict__ halo_dn, int fence_sys) {
   constexpr int V = 16 / sizeof(T);
   constexpr int TM = G * V * 256;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -380,6 +408,7 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   pdl_wait();  // from here on the previous kernel's writes are visible
+  bool halo_stored = false;  // stored into a neighbour's halo plane: fence before retiring
   auto issue = [&](int t) {
     const int s = t % nstages;
     int q = i0 - 1 + t;
@@ -449,8 +478,14 @@ __global__ void __launch_bounds__(256)
       }
       T *o = dst + (int64_t)i * M + m;
       st16<T>(o, out);
-      if (i == 0 && halo_up) st16<T>(halo_up + m, out);
-      if (i == rows - 1 && halo_dn) st16<T>(halo_dn + m, out);
+      if (i == 0 && halo_up) {
+        st16<T>(halo_up + m, out);
+        halo_stored = true;
+      }
+      if (i == rows - 1 && halo_dn) {
+        st16<T>(halo_dn + m, out);
+        halo_stored = true;
+      }
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         up[g][e] = cu[g][e];
@@ -464,6 +499,7 @@ __global__ void __launch_bounds__(256)
       issue(tn);
     }
   }
+  if (fence_sys && halo_stored) peer_fence();
 }
 
 // ================================================================================================
@@ -624,7 +660,7 @@ template <typename T, bool UNIT_D, int TJ, int MODE, bool WIDE>
 __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThreads, WIDE ? 1 : 2)
     k_fdtd_lf(const T *src, T *dst, int nx, int ny, int nz, int P, int64_t FS, int x0, int npl, int tiles,
               int chunks, int nstages, T c_h, T c_e, T d, T *halo_h, int64_t fs_h, T *halo_e,
-              int64_t fs_e) {
+              int64_t fs_e, int fence_sys) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int V = 16 / sizeof(T);
   constexpr int ER = TJ + 2, HR = TJ + 1;  // E rows / H rows per stage
@@ -661,6 +697,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
   }
   __syncthreads();
   pdl_wait();  // the previous iteration's writes are visible from here on
+  bool halo_stored = false;  // this thread stored into a neighbour's halo plane (fence at the end)
   uint32_t g_base = 0;  // stage uses so far (mbarrier phase bookkeeping across runs)
   for (int64_t u = u_begin; u < u_end;) {
     const int tile = (int)(u / nxp);
@@ -760,11 +797,12 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
           st16<T>(o + 3 * FS, hx);
           st16<T>(o + 4 * FS, hy);
           st16<T>(o + 5 * FS, hz);
-          if (halo_h && i == x0 + npl - 1) {  // slabs: my last plane -> the next slab's H halo
+          if (MODE != kLfFused && halo_h && i == x0 + npl - 1) {  // slabs: my last plane -> the next slab's H halo
             T *q = halo_h + (int64_t)jj * P + k0;
             st16<T>(q + 3 * fs_h, hx);
             st16<T>(q + 4 * fs_h, hy);
             st16<T>(q + 5 * fs_h, hz);
+            halo_stored = true;
           }
         }
       }
@@ -795,11 +833,12 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
           st16<T>(o, ex);
           st16<T>(o + FS, ey);
           st16<T>(o + 2 * FS, ez);
-          if (halo_e && i == x0) {  // slabs: my first plane -> the previous slab's E halo
+          if (MODE != kLfFused && halo_e && i == x0) {  // slabs: my first plane -> the previous slab's E halo
             T *q = halo_e + (int64_t)jj * P + k0;
             st16<T>(q, ex);
             st16<T>(q + fs_e, ey);
             st16<T>(q + 2 * fs_e, ez);
+            halo_stored = true;
           }
         }
 #pragma unroll
@@ -811,6 +850,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
     }
     g_base += (uint32_t)nload;
   }
+  if (fence_sys && halo_stored) peer_fence();
 }
 
 // ---- cross-process halo ordering (peer exchange, runtime.cu: ib_ipc_attach) -------------------------

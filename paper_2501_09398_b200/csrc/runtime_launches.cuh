@@ -71,15 +71,21 @@ const void *tma_fn(int G) {
   }
 }
 
-template <typename T, bool D3, int SH>
+template <typename T, bool D3, int SH, bool FS>
 const void *vec_fn_r(int R) {
-  return R >= 4 ? (const void *)ib::k_hotspot_vec<T, D3, 4, SH>
-                : R == 2 ? (const void *)ib::k_hotspot_vec<T, D3, 2, SH> : (const void *)ib::k_hotspot_vec<T, D3, 1, SH>;
+  return R >= 4 ? (const void *)ib::k_hotspot_vec<T, D3, 4, SH, FS>
+         : R == 2 ? (const void *)ib::k_hotspot_vec<T, D3, 2, SH, FS>
+                  : (const void *)ib::k_hotspot_vec<T, D3, 1, SH, FS>;
 }
+template <typename T, bool FS>
+const void *vec_fn_f(bool d3, int R, int sh) {
+  if (d3) return sh == 2 ? vec_fn_r<T, true, 2, FS>(R) : sh == 1 ? vec_fn_r<T, true, 1, FS>(R) : vec_fn_r<T, true, 0, FS>(R);
+  return sh ? vec_fn_r<T, false, 1, FS>(R) : vec_fn_r<T, false, 0, FS>(R);
+}
+// fs: the cross-process peer exchange's system-scope fence after halo stores (kernels.cuh)
 template <typename T>
-const void *vec_fn(bool d3, int R, int sh) {
-  if (d3) return sh == 2 ? vec_fn_r<T, true, 2>(R) : sh == 1 ? vec_fn_r<T, true, 1>(R) : vec_fn_r<T, true, 0>(R);
-  return sh ? vec_fn_r<T, false, 1>(R) : vec_fn_r<T, false, 0>(R);
+const void *vec_fn(bool d3, int R, int sh, bool fs) {
+  return fs ? vec_fn_f<T, true>(d3, R, sh) : vec_fn_f<T, false>(d3, R, sh);
 }
 
 template <typename T>
@@ -113,6 +119,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
       if (s.has_bot) dn = (T *)c->peer_buf_dn[parity ^ 1];
     }
     const int top = (int)s.has_top, bot = (int)s.has_bot;
+    const int fsys = (int)(c->dist() && c->peer);  // system-scope fence after halo stores (kernels.cuh)
     dim3 block(256);
     switch (hotspot_variant<T>(c, rows)) {
       case HotKernel::Vec: {
@@ -149,7 +156,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", 1);
         if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
         if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
-        const void *fn = vec_fn<T>(d3, (int)R, (int)std::min<int64_t>(sh, 2));
+        const void *fn = vec_fn<T>(d3, (int)R, (int)std::min<int64_t>(sh, 2), fsys != 0);
         dim3 grid((unsigned)xblocks, (unsigned)((rows + R * by - 1) / (R * by)));
         out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)by), g, src, dst, (const T *)s.power,
                                   rows, C, L, k, loss,
@@ -183,7 +190,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         rpc = std::min<int64_t>(rpc, rows);
         dim3 grid((unsigned)tiles, (unsigned)((rows + rpc - 1) / rpc));
         Launch Lz = make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, (int)rpc, ns,
-                                k, loss, top, bot, up, dn);
+                                k, loss, top, bot, up, dn, fsys);
         Lz.smem = smem;
         out.push_back(Lz);
         break;
@@ -193,7 +200,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         const int rpc = hotspot_rows_per_chunk(c, rows);
         dim3 grid((unsigned)((plane + 255) / 256), (unsigned)((rows + rpc - 1) / rpc));
         out.push_back(make_launch(fn, grid, block, g, src, dst, (const T *)s.power, rows, C, L, rpc, k,
-                                  loss, top, bot, up, dn));
+                                  loss, top, bot, up, dn, fsys));
       }
     }
   }
@@ -297,7 +304,7 @@ Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int
   }
   Launch L = make_launch(fn, dim3((unsigned)ctas), dim3((unsigned)threads), slab, (const T *)from, (T *)to, nx,
                          ny, nz, (int)c->lat_pitch, fs, x0, npl, (int)tiles, (int)chunks, cfg.ns, ch, ce, d,
-                         (T *)halo_h, fs_h, (T *)halo_e, fs_e);
+                         (T *)halo_h, fs_h, (T *)halo_e, fs_e, (int)(c->dist() && c->peer));
   L.smem = cfg.smem;
   L.step = mode == ib::kLfE ? 1 : 0;
   return L;
