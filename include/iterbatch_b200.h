@@ -103,7 +103,8 @@ int ib_mem_info(int device, int64_t *free_bytes, int64_t *total_bytes);
  *          (nx+1)-plane lattice the same way. Each slab's kernel stores its boundary plane(s)
  *          straight into the neighbours' halo planes (peer pointers between devices); cross-slab
  *          ordering is graph edges. Device ids may repeat (several slabs on one GPU, same graph).
- *          vector / fused fdtd require ndevices == 1. NULL/0 means {current device}.
+ *          Both FDTD solvers shard (the fused one ping-pongs each slab's planes). vector requires
+ *          ndevices == 1. NULL/0 means {current device}.
  * Device layout: vector and hotspot fields are C-order like the reference's arrays; both FDTD
  *          solvers keep the six fields on one padded (nx+1) x (ny+1) x P lattice (P = nz+1
  *          rounded up to 16 bytes), converted by ib_upload / ib_download.

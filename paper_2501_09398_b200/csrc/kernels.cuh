@@ -654,7 +654,9 @@ constexpr int lf_max_threads(int) { return kLfMaxThreads; }
 // needs no E_old(i+1) stage. In place is race-free: a CTA writes only its own rows, and the halo
 // rows it stages from a neighbour's tile are rows of the other field kind (not written by this
 // launch) or rows it never uses (H halo in the H launch, E halo in the E launch).
-constexpr int kLfFused = 0, kLfH = 1, kLfE = 2;
+// kLfFusedSlab: the fused leapfrog on one axis-0 slab of the lattice, with the halo pushes (a
+// separate instantiation: the halo code costs the halo-free kernel ~6% at 256^3).
+constexpr int kLfFused = 0, kLfH = 1, kLfE = 2, kLfFusedSlab = 3;
 
 template <typename T, bool UNIT_D, int TJ, int MODE, bool WIDE>
 __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThreads, WIDE ? 1 : 2)
@@ -664,6 +666,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int V = 16 / sizeof(T);
   constexpr int ER = TJ + 2, HR = TJ + 1;  // E rows / H rows per stage
+  constexpr bool FUSED = MODE == kLfFused || MODE == kLfFusedSlab;
   pdl_trigger();
   T *ring = reinterpret_cast<T *>(smem_raw);
   const int stage = 3 * (ER + HR) * P;  // elements per stage
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
         ld16<T>(hy, Hr + HR * P);
         ld16<T>(hz, Hr + 2 * HR * P);
       }
-      if (MODE != kLfE && row_ok && (MODE == kLfFused || r >= 1)) {
+      if (MODE != kLfE && row_ok && (FUSED || r >= 1)) {
         T exd[V], ezd[V], eyn[V], ezn[V];
         ld16<T>(exr, Ec);
         ld16<T>(eyr, Ec + ER * P);
@@ -787,7 +790,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
           hy[e] = (ilt && klt[e]) ? b : T(0);
           hz[e] = (ilt && jlt && kle[e]) ? c : T(0);
         }
-        if (MODE == kLfFused) {
+        if (FUSED) {
           st16<T>(Hr, hx);
           st16<T>(Hr + HR * P, hy);
           st16<T>(Hr + 2 * HR * P, hz);
@@ -838,6 +841,13 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
             st16<T>(q, ex);
             st16<T>(q + fs_e, ey);
             st16<T>(q + 2 * fs_e, ez);
+            halo_stored = true;
+          }
+          if (MODE == kLfFusedSlab && halo_h && i == x0 + npl - 1) {  // fused slabs: the next slab's seed
+            T *q = halo_h + (int64_t)jj * P + k0;                  // plane needs E too
+            st16<T>(q, ex);
+            st16<T>(q + fs_h, ey);
+            st16<T>(q + 2 * fs_h, ez);
             halo_stored = true;
           }
         }

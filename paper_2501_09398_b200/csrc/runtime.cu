@@ -100,10 +100,10 @@ void ib_destroy(ib_ctx *c) {
 static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   const int P = ndevices;
   const bool hot = c->solver == IB_SOLVER_HOTSPOT2D || c->solver == IB_SOLVER_HOTSPOT3D;
-  if (P > 1 && !hot && c->solver != IB_SOLVER_FDTD)
-    return fail(IB_EINVAL, "multi-slab execution is defined for the hotspot solvers and the two-half-step FDTD");
+  if (P > 1 && !hot && !c->fdtd())
+    return fail(IB_EINVAL, "multi-slab execution is defined for the hotspot and FDTD solvers");
   // axis-0 slabs: hotspot rows, or the FDTD lattice's nx+1 planes
-  const int64_t rows = hot ? c->dims[0] : (c->solver == IB_SOLVER_FDTD && (P > 1 || c->nranks > 1) ? c->dims[0] + 1 : 1);
+  const int64_t rows = hot ? c->dims[0] : (c->fdtd() && (P > 1 || c->nranks > 1) ? c->dims[0] + 1 : 1);
   if (P > rows) return fail(IB_EINVAL, "more slabs than rows along axis 0");
   c->slabs.resize(P);
   const bool dist = c->nranks > 1;
@@ -171,7 +171,8 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
     const bool fused = c->solver == IB_SOLVER_FDTD_FUSED;
     if (fused && lf_config(c).tj == 0)
       return fail(IB_EINVAL, "fused fdtd: the z rows are too long for one CTA (threads or shared-memory ring); use the two-kernel solver");
-    if (P > 1 || dist) {  // slabs / ranks: planes [lo, hi) plus one halo plane each side, in place
+    if (P > 1 || dist) {  // slabs / ranks: planes [lo, hi) plus one halo plane each side; the
+      // two half-steps update one copy in place, the fused leapfrog ping-pongs two
       if (lf_config(c).tj == 0)
         return fail(IB_EINVAL, "fdtd slabs need the staged kernel: the z rows are too long for one CTA");
       const int64_t plane = (ny + 1) * c->lat_pitch;
@@ -179,8 +180,10 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
         IB_CUDA(cudaSetDevice(s.device));
         s.fs = (int64_t)(s.rows() + 2) * plane;
         const size_t bb = (size_t)(6 * s.fs * es);
-        IB_CUDA(cudaMalloc(&s.buf[0], bb));
-        IB_CUDA(cudaMemset(s.buf[0], 0, bb));
+        for (int p = 0; p < (fused ? 2 : 1); ++p) {
+          IB_CUDA(cudaMalloc(&s.buf[p], bb));
+          IB_CUDA(cudaMemset(s.buf[p], 0, bb));
+        }
       }
       IB_CUDA(cudaSetDevice(c->slabs[0].device));
       IB_CUDA(cudaDeviceSynchronize());
@@ -551,7 +554,7 @@ static int xfer(ib_ctx *c, int field, void *host, size_t bytes, bool up) {
       fdtd_planes(c, s, field, up, &lo, &hi);
       if (hi <= lo) continue;
       char *hbase = (char *)host + (size_t)((lo - host0) * sh[1] * sh[2]) * es;
-      char *dbase = (char *)s.buf[0] + (size_t)(field * s.fs + (lo - s.row_lo + 1) * plane) * es;
+      char *dbase = (char *)s.buf[c->cur] + (size_t)(field * s.fs + (lo - s.row_lo + 1) * plane) * es;
       cudaMemcpy3DParms m = {};
       cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, (size_t)sh[2] * es, (size_t)sh[2] * es, (size_t)sh[1]);
       cudaPitchedPtr dp = make_cudaPitchedPtr(dbase, (size_t)c->lat_pitch * es, (size_t)sh[2] * es,

@@ -260,12 +260,18 @@ const void *lf_fn_w(int tj) {
 }
 template <typename T, bool U, int M>
 const void *lf_fn_m(int tj, bool wide) { return wide ? lf_fn_w<T, U, M, true>(tj) : lf_fn_w<T, U, M, false>(tj); }
+template <typename T, bool U>
+const void *lf_fn_u(int tj, int mode, bool wide) {
+  switch (mode) {
+    case ib::kLfH: return lf_fn_m<T, U, ib::kLfH>(tj, wide);
+    case ib::kLfE: return lf_fn_m<T, U, ib::kLfE>(tj, wide);
+    case ib::kLfFusedSlab: return lf_fn_m<T, U, ib::kLfFusedSlab>(tj, wide);
+    default: return lf_fn_m<T, U, ib::kLfFused>(tj, wide);
+  }
+}
 template <typename T>
 const void *lf_fn(bool unit, int tj, int mode, bool wide) {
-  if (unit) return mode == ib::kLfH ? lf_fn_m<T, true, ib::kLfH>(tj, wide)
-                   : mode == ib::kLfE ? lf_fn_m<T, true, ib::kLfE>(tj, wide) : lf_fn_m<T, true, ib::kLfFused>(tj, wide);
-  return mode == ib::kLfH ? lf_fn_m<T, false, ib::kLfH>(tj, wide)
-         : mode == ib::kLfE ? lf_fn_m<T, false, ib::kLfE>(tj, wide) : lf_fn_m<T, false, ib::kLfFused>(tj, wide);
+  return unit ? lf_fn_u<T, true>(tj, mode, wide) : lf_fn_u<T, false>(tj, mode, wide);
 }
 
 // One k_fdtd_lf launch of `mode` from lattice buffer `from` to `to` (equal for the in-place
@@ -385,8 +391,35 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
 // FDTD fused: one k_fdtd_lf launch per iteration, parity -> parity ^ 1.
 template <typename T>
 void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
-  out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1], 0, (int)c->dims[0] + 1,
-                             c->lat_fs));
+  const int P = (int)c->slabs.size();
+  if (P == 1) {
+    out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1], 0, (int)c->dims[0] + 1,
+                               c->lat_fs));
+    return;
+  }
+  // axis-0 slabs of the lattice, ping-pong per slab: slab g reads buf[parity] (its planes and the
+  // halo plane each side) and writes buf[parity ^ 1]; its kernel stores its last plane's new E and
+  // H into slab g+1's lower halo (that slab's seed plane) and its first plane's new E into slab
+  // g-1's upper halo (the E_old(i+1) of that slab's last plane), both in buf[parity ^ 1].
+  const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lattice_pitch();
+  for (int g = 0; g < P; ++g) {
+    Slab &s = c->slabs[g];
+    const int64_t off = (int64_t)(1 - s.row_lo) * plane;  // global plane index addresses the buffer
+    T *src = (T *)s.buf[parity] + off, *dst = (T *)s.buf[parity ^ 1] + off;
+    void *hh = nullptr, *he = nullptr;
+    int64_t fh = 0, fe = 0;
+    if (g + 1 < P) {
+      Slab &n = c->slabs[g + 1];
+      hh = n.buf[parity ^ 1];  // its lower halo plane (local 0)
+      fh = n.fs;
+    }
+    if (g > 0) {
+      Slab &n = c->slabs[g - 1];
+      he = (T *)n.buf[parity ^ 1] + (int64_t)(n.rows() + 1) * plane;  // its upper halo plane
+      fe = n.fs;
+    }
+    out.push_back(lf_launch<T>(c, ib::kLfFusedSlab, src, dst, s.row_lo, s.rows(), s.fs, hh, fh, he, fe, g));
+  }
 }
 
 void iteration_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {

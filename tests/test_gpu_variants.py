@@ -242,6 +242,39 @@ def test_fdtd_fused_non_unit_cell_size(gpu, env, ctas):
 @pytest.mark.parametrize("slabs", [2, 3, 5])
 @pytest.mark.parametrize("dims", [(8, 4, 8), (16, 9, 33), (5, 6, 7), (40, 9, 70)],
                          ids=["8x4x8", "16x9x33", "5x6x7", "40x9x70"])
+def test_fused_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
+    """The fused leapfrog split into axis-0 lattice slabs (each slab ping-pongs its planes plus a
+    halo plane each side; the kernel stores its last plane's new E and H into the next slab's
+    seed plane and its first plane's new E into the previous slab's upper halo) == one domain ==
+    the oracle, bit for bit: graph (capture) at even and odd K, stream mode, tile / chunk
+    variants."""
+    if slabs > dims[0] + 1:
+        pytest.skip("more slabs than planes")
+    base = wl.fdtd_cavity(*dims)
+    rng = np.random.default_rng(100 + sum(dims) + slabs)
+    state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
+                            base.cell_size, base.time_step)
+    npd = np.float32 if dtype == "f32" else np.float64
+    dt = state.time_step
+    want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
+                     dt / wl.VACUUM_PERMITTIVITY, 6, npd)
+    devs = [0] * slabs
+    for tj, chunks in ((0, 0), (1, 2), (3, 1)):
+        env(IB_FDTD_TJ=tj, IB_FDTD_CHUNKS=chunks)
+        for k, n in ((3, 2), (2, 3)):
+            got = wl.run_batched(wl.fdtd_program(), state, k, n, dtype=dtype, devices=devs, build="capture",
+                                 fuse=True)
+            for g, w in zip(got.state_arrays(), want):
+                assert np.array_equal(np.asarray(g, npd), w), (tj, chunks, k)
+        got = wl.run_loop(wl.fdtd_program(), state, 6, dtype=dtype, devices=devs, fuse=True)
+        for g, w in zip(got.state_arrays(), want):
+            assert np.array_equal(np.asarray(g, npd), w), (tj, chunks)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("slabs", [2, 3, 5])
+@pytest.mark.parametrize("dims", [(8, 4, 8), (16, 9, 33), (5, 6, 7), (40, 9, 70)],
+                         ids=["8x4x8", "16x9x33", "5x6x7", "40x9x70"])
 def test_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
     """FDTD split into axis-0 slabs of the lattice (halo planes pushed by the H / E launches
     into the neighbours, cross-slab graph edges) == one domain == the oracle, bit for bit, in
