@@ -192,7 +192,8 @@ uint64_t ib_fnv1a64_f64(const void *values, size_t n, int dtype, uint64_t h);
  * For these contexts ib_upload takes the slab WITH its halo rows, i.e. global rows
  * [lo - has_top, hi + has_bot) for the temperature and [lo, hi) for the power; ib_download
  * returns the owned rows [lo, hi). ib_slab_info reports lo, hi, has_top, has_bot.
- * IB_SOLVER_FDTD (peer exchange only): a rank owns planes [lo, hi) of the (nx+1)-plane lattice;
+ * IB_SOLVER_FDTD and IB_SOLVER_FDTD_FUSED (peer exchange only; id128 must be NULL): a rank owns
+ * planes [lo, hi) of the (nx+1)-plane lattice;
  * for every field ib_upload takes its global planes [lo - has_top, hi + has_bot) and ib_download
  * returns [lo, hi), both clipped to that field's own extent along axis 0 (nx or nx+1). */
 int ib_nccl_unique_id(void *id128);

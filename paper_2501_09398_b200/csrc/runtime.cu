@@ -107,8 +107,8 @@ static int create_impl(ib_ctx *c, const int *devices, int ndevices) {
   if (P > rows) return fail(IB_EINVAL, "more slabs than rows along axis 0");
   c->slabs.resize(P);
   const bool dist = c->nranks > 1;
-  if (dist && (P != 1 || !(hot || c->solver == IB_SOLVER_FDTD)))
-    return fail(IB_EINVAL, "distributed contexts are single-slab hotspot or two-half-step FDTD grids");
+  if (dist && (P != 1 || !(hot || c->fdtd())))
+    return fail(IB_EINVAL, "distributed contexts are single-slab hotspot or FDTD grids");
   if (dist && c->nranks > rows) return fail(IB_EINVAL, "more ranks than rows along axis 0");
   for (int g = 0; g < P; ++g) {
     Slab &s = c->slabs[g];
@@ -328,10 +328,10 @@ int ib_nccl_unique_id(void *id128) {
 int ib_create_dist(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndims,
                    const double *scalars, int nscalars, int device, int rank, int nranks,
                    const void *id128) {
-  if (solver != IB_SOLVER_HOTSPOT2D && solver != IB_SOLVER_HOTSPOT3D && solver != IB_SOLVER_FDTD)
-    return fail(IB_EINVAL, "distributed contexts are defined for hotspot grids and the two-half-step FDTD");
+  if (solver == IB_SOLVER_VECTOR)
+    return fail(IB_EINVAL, "distributed contexts are defined for hotspot grids and FDTD");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(IB_EINVAL, "bad rank / nranks");
-  if (solver == IB_SOLVER_FDTD && nranks > 1 && id128)
+  if ((solver == IB_SOLVER_FDTD || solver == IB_SOLVER_FDTD_FUSED) && nranks > 1 && id128)
     return fail(IB_EINVAL, "distributed FDTD uses the peer exchange: pass id128 = NULL, then ib_ipc_attach");
 
   return create_common(out, solver, dtype, dims, ndims, scalars, nscalars, &device, 1, rank, nranks,
@@ -365,7 +365,7 @@ int ib_ipc_attach(ib_ctx *c, const void *up, const void *dn) {
   auto open = [&](const void *blob, void **bufs, unsigned long long **sync) -> int {
     cudaIpcMemHandle_t h[3];
     std::memcpy(h, blob, sizeof(h));
-    for (int p = 0; p < (c->fdtd() ? 1 : 2); ++p)
+    for (int p = 0; p < (c->solver == IB_SOLVER_FDTD ? 1 : 2); ++p)  // in-place FDTD: one lattice
       IB_CUDA(cudaIpcOpenMemHandle(&bufs[p], h[p], cudaIpcMemLazyEnablePeerAccess));
     void *sp = nullptr;
     IB_CUDA(cudaIpcOpenMemHandle(&sp, h[2], cudaIpcMemLazyEnablePeerAccess));

@@ -392,7 +392,7 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
 template <typename T>
 void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
   const int P = (int)c->slabs.size();
-  if (P == 1) {
+  if (P == 1 && !c->dist()) {
     out.push_back(lf_launch<T>(c, ib::kLfFused, c->lat[parity], c->lat[parity ^ 1], 0, (int)c->dims[0] + 1,
                                c->lat_fs));
     return;
@@ -402,6 +402,23 @@ void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
   // H into slab g+1's lower halo (that slab's seed plane) and its first plane's new E into slab
   // g-1's upper halo (the E_old(i+1) of that slab's last plane), both in buf[parity ^ 1].
   const int64_t plane = (int64_t)(c->dims[1] + 1) * c->lattice_pitch();
+  if (c->dist()) {  // one rank's slab; the neighbour ranks' buffers through IPC mappings
+    Slab &s = c->slabs[0];
+    const int64_t off = (int64_t)(1 - s.row_lo) * plane;
+    void *hh = nullptr, *he = nullptr;
+    int64_t fh = 0, fe = 0;
+    if (c->peer && s.has_bot) {
+      hh = c->peer_buf_dn[parity ^ 1];  // the down rank's lower halo plane (its local 0)
+      fh = (int64_t)(c->peer_rows_dn + 2) * plane;
+    }
+    if (c->peer && s.has_top) {
+      he = (T *)c->peer_buf_up[parity ^ 1] + (int64_t)(c->peer_rows_up + 1) * plane;  // its upper halo
+      fe = (int64_t)(c->peer_rows_up + 2) * plane;
+    }
+    out.push_back(lf_launch<T>(c, ib::kLfFusedSlab, (T *)s.buf[parity] + off, (T *)s.buf[parity ^ 1] + off,
+                               s.row_lo, s.rows(), s.fs, hh, fh, he, fe, 0));
+    return;
+  }
   for (int g = 0; g < P; ++g) {
     Slab &s = c->slabs[g];
     const int64_t off = (int64_t)(1 - s.row_lo) * plane;  // global plane index addresses the buffer

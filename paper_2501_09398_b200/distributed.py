@@ -99,10 +99,13 @@ class DistributedSolver(DeviceSolver):
     """
 
     def __init__(self, state, dtype, rank: int, world: int, device: int, uid: bytes | None = None,
-                 upload: bool = True, exchange: str = "nccl", allgather=None):
+                 upload: bool = True, exchange: str = "nccl", allgather=None, fuse: bool = False):
         kind = _kind_of_state(state)
         if kind not in ("hotspot2d", "hotspot3d", "fdtd"):
             raise ValueError("distributed execution is defined for hotspot grids and FDTD")
+        if fuse and kind != "fdtd":
+            raise ValueError("fuse=True applies to FDTD (H and E half-steps in one kernel)")
+        self.fused = bool(fuse)
         if kind == "fdtd" and world > 1 and exchange != "peer":
             raise ValueError("distributed FDTD uses exchange='peer'")
         self.kind = kind
@@ -130,7 +133,8 @@ class DistributedSolver(DeviceSolver):
             idp = ctypes.cast(self._uid, ctypes.c_void_p)
         if world > 1 and exchange == "peer" and allgather is None:
             raise ValueError("exchange='peer' needs an allgather callable for the IPC handles")
-        _lib.check(L.ib_create_dist(ctypes.byref(ctx), _lib.SOLVER[kind], _lib.DTYPE[self.dtype], dims,
+        _lib.check(L.ib_create_dist(ctypes.byref(ctx), _lib.SOLVER["fdtd_fused" if self.fused else kind],
+                                    _lib.DTYPE[self.dtype], dims,
                                     len(self.dims), sc, len(self.scalars), device, rank, world, idp))
         self._ctx = ctx
         self._allgather = allgather if (world > 1 and exchange == "peer") else None

@@ -20,7 +20,7 @@ The boundary is per RUN: a run uploads the state once, keeps it in HBM for all i
 downloads it once. ``workers`` is accepted for signature compatibility and ignored (the device
 grid replaces the row-slab threads). Keyword-only extensions: ``dtype`` ("f64" reproduces the
 reference bit for bit; "f32" is the bandwidth-halving mode, parity tiers in DESIGN.md), ``devices``
-(axis-0 slabs for hotspot grids and the two-half-step FDTD), and graph options (``build``, ``pdl``, ``while_loop``).
+(axis-0 slabs for hotspot grids and both FDTD solvers), and graph options (``build``, ``pdl``, ``while_loop``).
 
 There is no CPU fallback: without the library or a CUDA device every call raises.
 Reference dataclasses are accepted too (duck-typed); results come back as the input's type.

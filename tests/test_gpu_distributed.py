@@ -166,7 +166,7 @@ def _fdtd_state(dims, seed=11):
                            base.time_step)
 
 
-def _rank_main_fdtd(rank, world, port, dims, dtype, q):
+def _rank_main_fdtd(rank, world, port, dims, dtype, q, fuse=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), IB_DIST_TIMEOUT_MS="60000")
@@ -180,7 +180,7 @@ def _rank_main_fdtd(rank, world, port, dims, dtype, q):
         st = _fdtd_state(dims)
         device = rank % _lib.device_count()
         d = DistributedSolver(st, dtype, rank=rank, world=world, device=device, exchange="peer",
-                              allgather=allgather)
+                              allgather=allgather, fuse=fuse)
         d.run_batched(3, 2)   # graph: per half-step wait / H or E with halo stores / signal
         d.run_stream(1)       # stream mode
         parts = [None] * world
@@ -196,17 +196,19 @@ def _rank_main_fdtd(rank, world, port, dims, dtype, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fuse", [False, True], ids=["two-half-steps", "fused"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("world,dims", [(2, (8, 4, 8)), (3, (16, 9, 33)), (2, (5, 6, 7))])
-def test_multi_rank_fdtd_peer_equals_single_domain(gpu, world, dims, dtype):
-    """FDTD lattice split into one slab per process, H / E halo planes stored into the
-    neighbours' buffers through CUDA IPC with per-half-step counter ordering == one domain."""
+def test_multi_rank_fdtd_peer_equals_single_domain(gpu, world, dims, dtype, fuse):
+    """FDTD lattice split into one slab per process, halo planes stored into the neighbours'
+    buffers through CUDA IPC with counter ordering (per half-step; per iteration for the fused
+    leapfrog, whose slabs ping-pong) == one domain."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main_fdtd, args=(r, world, port, dims, dtype, q))
+    procs = [ctx.Process(target=_rank_main_fdtd, args=(r, world, port, dims, dtype, q, fuse))
              for r in range(world)]
     for p in procs:
         p.start()
