@@ -635,8 +635,11 @@ __global__ void __launch_bounds__(256)
 // refilled. A launch covers planes [x0, x0 + npl) (global indices; src / dst are pre-offset so
 // global plane indices address the buffer): the whole lattice, or one axis-0 slab of it. Slabs
 // (two half-step solver): the H launch also stores its last plane's H into the next slab's halo
-// plane (halo_h), the E launch its first plane's E into the previous slab's (halo_e) — device-
-// local or peer pointers; ordering is the launch layer's cross-slab graph edges. Masks are branch-free selects; a run starting at x0 > 0 first recomputes H_new(x0-1)
+// plane (halo_h), the E launch its first plane's E into the previous slab's (halo_e); fused
+// slabs (kLfFusedSlab, ping-pong): the last plane's new E and H into the next slab's seed plane
+// (halo_h), the first plane's new E into the previous slab's upper halo (halo_e) — device-local
+// or peer pointers; ordering is the launch layer's cross-slab graph edges (or, across processes,
+// the k_dist_wait / k_dist_signal counters after a system-scope fence, fence_sys). Masks are branch-free selects; a run starting at x0 > 0 first recomputes H_new(x0-1)
 // without writing, to seed the carry.
 // ================================================================================================
 // (TJ+1) x groups-per-row threads, rounded up to warps; two CTAs per SM must fit the register file.
