@@ -20,7 +20,9 @@ The boundary is per RUN: a run uploads the state once, keeps it in HBM for all i
 downloads it once. ``workers`` is accepted for signature compatibility and ignored (the device
 grid replaces the row-slab threads). Keyword-only extensions: ``dtype`` ("f64" reproduces the
 reference bit for bit; "f32" is the bandwidth-halving mode, parity tiers in DESIGN.md), ``devices``
-(axis-0 slabs for hotspot grids and both FDTD solvers), and graph options (``build``, ``pdl``, ``while_loop``).
+(axis-0 slabs for hotspot grids and both FDTD solvers; ``halo="copy"`` moves hotspot halo planes
+with peer-copy nodes instead of the kernel's own stores), ``fuse`` (FDTD: H and E in one kernel),
+and graph options (``build``, ``pdl``, ``while_loop``, ``patch``).
 
 There is no CPU fallback: without the library or a CUDA device every call raises.
 Reference dataclasses are accepted too (duck-typed); results come back as the input's type.
@@ -550,19 +552,19 @@ _CACHE: "OrderedDict[tuple, DeviceSolver]" = OrderedDict()
 _CACHE_SIZE = 2
 
 
-def _solver_for(state, dtype, devices, fuse: bool = False) -> DeviceSolver:
+def _solver_for(state, dtype, devices, fuse: bool = False, halo: str = "store") -> DeviceSolver:
     """A (cached) device context for this state's shape, with the state uploaded."""
     kind = _kind_of_state(state)
     dt = _norm_dtype(dtype)
     dims, scalars = _dims_scalars(kind, state)
     devs = tuple(devices) if devices else ()
-    key = (kind, dt, dims, scalars, devs, bool(fuse))
+    key = (kind, dt, dims, scalars, devs, bool(fuse), halo)
     s = _CACHE.pop(key, None)
     if s is None:
         while len(_CACHE) >= _CACHE_SIZE:
             _, old = _CACHE.popitem(last=False)
             old.close()
-        s = DeviceSolver(state, dt, devs, upload=False, fuse=fuse)
+        s = DeviceSolver(state, dt, devs, upload=False, fuse=fuse, halo=halo)
     _CACHE[key] = s
     s.upload(state)
     return s
@@ -663,7 +665,7 @@ def _check_program(program, state) -> str:
 # Drivers
 # ================================================================================================
 def run_loop(program, state, total_iterations: int, workers=None, *, dtype="f64", devices=None,
-             pdl: bool = False, fuse: bool = False):
+             pdl: bool = False, fuse: bool = False, halo: str = "store"):
     """Apply the program total_iterations times, one launch at a time (Listing 1).
 
     Mirrors workloads.py:442-450: N = 0 returns the same state; N < 0 raises ValueError.
@@ -674,14 +676,14 @@ def run_loop(program, state, total_iterations: int, workers=None, *, dtype="f64"
     _check_program(program, state)
     if total == 0:
         return state
-    s = _solver_for(state, dtype, devices, fuse)
+    s = _solver_for(state, dtype, devices, fuse, halo)
     s.run_stream(total, pdl=pdl)
     return s.download(state, fields=_written_fields(state))
 
 
 def run_batched(program, state, batch_size: int, num_batches: int, workers=None, *, dtype="f64",
                 devices=None, build: str = "manual", pdl: bool = False, while_loop: bool = False,
-                fuse: bool = False, patch: bool = False):
+                fuse: bool = False, patch: bool = False, halo: str = "store"):
     """Apply the program in num_batches replays of a batch_size-iteration CUDA graph (Listing 3).
 
     Mirrors workloads.py:453-471 (batch_size < 1 or num_batches < 0 raise ValueError) and
@@ -696,7 +698,7 @@ def run_batched(program, state, batch_size: int, num_batches: int, workers=None,
     _check_program(program, state)
     if num == 0:
         return state
-    s = _solver_for(state, dtype, devices, fuse)
+    s = _solver_for(state, dtype, devices, fuse, halo)
     s.build_graph(size, build=build, pdl=pdl, while_loop=while_loop, patch=patch)
     s.run_graph(num)
     s.destroy_graph()
@@ -704,7 +706,8 @@ def run_batched(program, state, batch_size: int, num_batches: int, workers=None,
 
 
 def run_peeled(program, state, total_iterations: int, batch_size: int, workers=None, *,
-               dtype="f64", devices=None, build: str = "manual", pdl: bool = False, fuse: bool = False):
+               dtype="f64", devices=None, build: str = "manual", pdl: bool = False, fuse: bool = False,
+               halo: str = "store"):
     """Any total_iterations with any batch_size: floor(N/K) graph replays plus a remainder graph.
 
     Loop peeling, the paper's remedy for the divisibility restriction that the
@@ -719,7 +722,7 @@ def run_peeled(program, state, total_iterations: int, batch_size: int, workers=N
     _check_program(program, state)
     if total == 0:
         return state
-    s = _solver_for(state, dtype, devices, fuse)
+    s = _solver_for(state, dtype, devices, fuse, halo)
     s.run_peeled(total, size, build=build, pdl=pdl)
     return s.download(state, fields=_written_fields(state))
 

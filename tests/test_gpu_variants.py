@@ -120,6 +120,9 @@ def test_hotspot_slabs_copy_exchange(gpu, env, kernel, slabs):
                 s.upload(state)
                 s.run_batched(k, n, build="capture", pdl=True)
                 assert np.array_equal(s.download(state).temperature, want), (shape, k)
+        got = wl.run_batched(wl.hotspot_program(), state, 3, 2, devices=[0] * slabs, build="capture",
+                             halo="copy")  # the module-level drivers take the option too
+        assert np.array_equal(got.temperature, want), shape
         with wl.DeviceSolver(state, "f32", devices=[0] * slabs, halo="copy") as s, \
                 wl.DeviceSolver(state, "f32", devices=[0] * slabs) as v2:
             s.run_batched(3, 2, build="capture")
