@@ -333,7 +333,7 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
             exec_s.append(solver.run_graph(num).gpu_s)
         solver.destroy_graph()
         stream_s = []
-        for _ in range(3):
+        for _ in range(5):  # the host's launch rate varies run to run: 5 samples for the error bar
             solver.flush_l2()
             stream_s.append(solver.run_stream(n).gpu_s)
         stream_pdl = []
