@@ -113,12 +113,13 @@ int ib_create(ib_ctx **out, int solver, int dtype, const int64_t *dims, int ndim
               const double *scalars, int nscalars, const int *devices, int ndevices);
 void ib_destroy(ib_ctx *ctx);
 
-/* Halo exchange of a multi-slab hotspot context (ib_create with ndevices > 1), SURVEY.md §8e:
- * IB_HALO_STORE (default, v2) — each slab's stencil kernel stores its boundary planes straight into
- * the neighbours' halo planes; IB_HALO_COPY (v1) — the kernel writes only its own slab and one
- * peer cudaMemcpyAsync (UVA) per face follows it on the slab's stream (memcpy nodes in the captured
- * graph). Same results bit for bit. Drops any built graph. EINVAL for other solvers / contexts
- * (FDTD slabs, ib_create_dist). Single-slab contexts accept either and ignore it. */
+/* Halo exchange of a multi-slab context (ib_create with ndevices > 1), SURVEY.md §8e:
+ * IB_HALO_STORE (default, v2) — each slab's kernel stores its boundary planes straight into the
+ * neighbours' halo planes; IB_HALO_COPY (v1) — the kernels write only their own slab and peer
+ * cudaMemcpyAsync (UVA) copies of those planes follow each launch on the slab's stream (memcpy
+ * nodes in the captured graph; FDTD: the H / E / fused planes each neighbour reads). Same results
+ * bit for bit. Drops any built graph. EINVAL for distributed (ib_create_dist) contexts.
+ * Single-slab contexts accept either and ignore it. */
 #define IB_HALO_STORE 0
 #define IB_HALO_COPY 1
 int ib_set_halo_mode(ib_ctx *ctx, int mode);

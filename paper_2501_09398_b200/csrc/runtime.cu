@@ -672,7 +672,7 @@ int ib_run_step(ib_ctx *c, int step, ib_times *tm) {
     Slab &s = c->slabs[L.slab];
     IB_CUDA(cudaSetDevice(s.device));
     IB_TRY(launch_one(L, s.stream, false));
-    if (copies_halos(c)) IB_TRY(halo_copies(c, L.slab, c->cur ^ 1, s.stream));
+    if (copies_halos(c)) IB_TRY(halo_copies(c, L.slab, c->cur ^ 1, L.step, s.stream));
     ++t.kernels;
   }
   IB_TRY(join_into(c, c->stream(), false));
@@ -694,8 +694,8 @@ int ib_set_halo_mode(ib_ctx *c, int mode) {
   IB_TRY(check_ctx(c));
   if (mode != IB_HALO_STORE && mode != IB_HALO_COPY)
     return fail(IB_EINVAL, "halo mode must be IB_HALO_STORE or IB_HALO_COPY");
-  if (mode == IB_HALO_COPY && (c->dist() || (c->slabs.size() > 1 && !c->hotspot())))
-    return fail(IB_EINVAL, "IB_HALO_COPY applies to single-process hotspot slabs only");
+  if (mode == IB_HALO_COPY && c->dist())
+    return fail(IB_EINVAL, "IB_HALO_COPY applies to single-process slabs (ranks exchange by peer stores or NCCL)");
   if (c->halo_copy != (mode == IB_HALO_COPY)) {
     DeviceGuard guard;
     IB_CUDA(cudaSetDevice(c->slabs[0].device));

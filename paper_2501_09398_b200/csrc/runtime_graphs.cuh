@@ -60,27 +60,50 @@ int launch_dist_signal(ib_ctx *c, cudaStream_t st) {
   return launch_one(L, st, false);
 }
 
-// IB_HALO_COPY: slab g's first / last owned plane of an iteration's output
-// buf[outpar] into the neighbours' halo planes, one peer copy per face on slab g's stream right
-// after its kernel: cudaMemcpyAsync over UVA (peer access is enabled between slab devices;
-// cudaMemcpyPeerAsync cannot be captured), a memcpy node in the graph. Slab buffers are (rows + 2) planes:
-// top halo, owned rows, bottom halo.
-int halo_copies(ib_ctx *c, int g, int outpar, cudaStream_t st) {
+// IB_HALO_COPY: the halo planes a slab's launch would have stored into its
+// neighbours, moved by peer copies on the slab's stream right after the launch — cudaMemcpyAsync
+// over UVA (peer access is enabled between slab devices; cudaMemcpyPeerAsync cannot be stream-
+// captured), memcpy nodes in the graph, before the slab's "done" event, so the same phase edges
+// order them. Slab buffers hold one halo plane each side: local plane 0, owned 1..rows, rows+1.
+//   hotspot (ping-pong): my first / last owned output plane -> the neighbours' halos, buf[outpar]
+//   FDTD H launch (in place): my last plane's H (fields 3..5) -> the next slab's lower halo
+//   FDTD E launch (in place): my first plane's E (fields 0..2) -> the previous slab's upper halo
+//   fused FDTD (ping-pong): my last plane's E and H -> the next slab's lower halo, my first
+//                           plane's E -> the previous slab's upper halo, buf[outpar]
+int halo_copies(ib_ctx *c, int g, int outpar, int step, cudaStream_t st) {
   const int P = (int)c->slabs.size();
   Slab &s = c->slabs[g];
-  const size_t pb = (size_t)c->plane() * c->esize;
-  const char *b = (const char *)s.buf[outpar];
-  if (g > 0) {
-    Slab &n = c->slabs[g - 1];
-    IB_CUDA(cudaMemcpyAsync((char *)n.buf[outpar] + (size_t)(n.rows() + 1) * pb, b + pb, pb, cudaMemcpyDefault, st));
+  const size_t es = (size_t)c->esize;
+  if (c->hotspot()) {
+    const size_t pb = (size_t)c->plane() * es;
+    const char *b = (const char *)s.buf[outpar];
+    if (g > 0) {
+      Slab &n = c->slabs[g - 1];
+      IB_CUDA(cudaMemcpyAsync((char *)n.buf[outpar] + (size_t)(n.rows() + 1) * pb, b + pb, pb, cudaMemcpyDefault, st));
+    }
+    if (g + 1 < P) {
+      Slab &n = c->slabs[g + 1];
+      IB_CUDA(cudaMemcpyAsync(n.buf[outpar], b + (size_t)s.rows() * pb, pb, cudaMemcpyDefault, st));
+    }
+    return IB_OK;
   }
-  if (g + 1 < P) {
-    Slab &n = c->slabs[g + 1];
-    IB_CUDA(cudaMemcpyAsync(n.buf[outpar], b + (size_t)s.rows() * pb, pb, cudaMemcpyDefault, st));
-  }
+  const bool fused = c->solver == IB_SOLVER_FDTD_FUSED;
+  const int buf = fused ? outpar : 0;
+  const size_t pb = (size_t)(c->dims[1] + 1) * (size_t)c->lattice_pitch() * es;  // one field's plane
+  auto copy = [&](Slab &n, int64_t nplane, int64_t myplane, int f0, int f1) -> int {
+    for (int f = f0; f < f1; ++f)
+      IB_CUDA(cudaMemcpyAsync((char *)n.buf[buf] + ((size_t)f * n.fs * es + (size_t)nplane * pb),
+                              (const char *)s.buf[buf] + ((size_t)f * s.fs * es + (size_t)myplane * pb), pb,
+                              cudaMemcpyDefault, st));
+    return IB_OK;
+  };
+  if (g + 1 < P && (fused || step == 0))  // last plane -> next slab's lower halo (H; fused: E too)
+    IB_TRY(copy(c->slabs[g + 1], 0, s.rows(), fused ? 0 : 3, 6));
+  if (g > 0 && (fused || step == 1))  // first plane's E -> previous slab's upper halo
+    IB_TRY(copy(c->slabs[g - 1], c->slabs[g - 1].rows() + 1, 1, 0, 3));
   return IB_OK;
 }
-bool copies_halos(const ib_ctx *c) { return c->halo_copy && c->slabs.size() > 1 && c->hotspot(); }
+bool copies_halos(const ib_ctx *c) { return c->halo_copy && c->slabs.size() > 1 && !c->dist(); }
 
 // Enqueue `iters` iterations starting at `parity` onto the slab streams (also used under stream
 // capture). Multi-slab: kernel(g,t) waits for kernel(g+-1,t-1) — RAW on the halo it reads and
@@ -118,7 +141,7 @@ int enqueue_iterations(ib_ctx *c, int64_t iters, int parity, bool pdl, cudaStrea
       c->ev(single_stream ? IB_EV_NODE_ADDED : IB_EV_BASELINE_KERNEL_LAUNCHED, single_stream ? -1 : t,
             single_stream ? nk : (int64_t)q);
       IB_TRY(launch_one(L, st, use_pdl));
-      if (copies_halos(c)) IB_TRY(halo_copies(c, L.slab, par ^ 1, st));
+      if (copies_halos(c)) IB_TRY(halo_copies(c, L.slab, par ^ 1, L.step, st));
       if (P > 1) IB_CUDA(cudaEventRecord(s.ev[f & 1], st));
       if (c->peer) IB_TRY(launch_dist_signal(c, st));  // its halo planes went out with its stores
       ++nk;

@@ -356,11 +356,11 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
         T *base = (T *)s.buf[0] + (int64_t)(1 - s.row_lo) * plane;  // global plane index -> buffer
         void *hh = nullptr, *he = nullptr;
         int64_t fh = 0, fe = 0;
-        if (step == 0 && g + 1 < P) {
+        if (step == 0 && g + 1 < P && !c->halo_copy) {  // IB_HALO_COPY: copy nodes instead
           hh = c->slabs[g + 1].buf[0];  // its top halo plane (local 0)
           fh = c->slabs[g + 1].fs;
         }
-        if (step == 1 && g > 0) {
+        if (step == 1 && g > 0 && !c->halo_copy) {
           Slab &n = c->slabs[g - 1];
           he = (T *)n.buf[0] + (int64_t)(n.rows() + 1) * plane;  // its bottom halo plane
           fe = n.fs;
@@ -425,12 +425,12 @@ void fdtd_fused_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     T *src = (T *)s.buf[parity] + off, *dst = (T *)s.buf[parity ^ 1] + off;
     void *hh = nullptr, *he = nullptr;
     int64_t fh = 0, fe = 0;
-    if (g + 1 < P) {
+    if (g + 1 < P && !c->halo_copy) {  // IB_HALO_COPY: copy nodes instead (runtime_graphs.cuh)
       Slab &n = c->slabs[g + 1];
       hh = n.buf[parity ^ 1];  // its lower halo plane (local 0)
       fh = n.fs;
     }
-    if (g > 0) {
+    if (g > 0 && !c->halo_copy) {
       Slab &n = c->slabs[g - 1];
       he = (T *)n.buf[parity ^ 1] + (int64_t)(n.rows() + 1) * plane;  // its upper halo plane
       fe = n.fs;

@@ -137,8 +137,8 @@ def test_halo_mode_validation(gpu):
         wl.DeviceSolver(hot, "f32", halo="nvlink")
     with wl.DeviceSolver(hot, "f32", halo="copy") as s:  # one slab: accepted, nothing to exchange
         s.run_stream(2)
-    with pytest.raises(ValueError):
-        wl.DeviceSolver(wl.fdtd_cavity(6, 4, 6), "f32", devices=[0, 0], halo="copy")
+    with wl.DeviceSolver(wl.fdtd_cavity(6, 4, 6), "f32", devices=[0, 0], halo="copy") as s:
+        s.run_stream(2)  # FDTD slabs take the copy exchange too
 
 
 FDTD_DIMS = [(8, 4, 8), (5, 6, 7), (1, 1, 1), (3, 1, 9), (16, 9, 33), (2, 40, 3)]
@@ -272,6 +272,13 @@ def test_fused_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
         got = wl.run_loop(wl.fdtd_program(), state, 6, dtype=dtype, devices=devs, fuse=True)
         for g, w in zip(got.state_arrays(), want):
             assert np.array_equal(np.asarray(g, npd), w), (tj, chunks)
+    env(IB_FDTD_TJ=0, IB_FDTD_CHUNKS=0)
+    for run in (lambda: wl.run_batched(wl.fdtd_program(), state, 3, 2, dtype=dtype, devices=devs,
+                                       build="capture", fuse=True, halo="copy"),
+                lambda: wl.run_loop(wl.fdtd_program(), state, 6, dtype=dtype, devices=devs, fuse=True,
+                                    halo="copy")):
+        for g, w in zip(run().state_arrays(), want):  # IB_HALO_COPY: peer-copy nodes move the halos
+            assert np.array_equal(np.asarray(g, npd), w)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
@@ -301,3 +308,9 @@ def test_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
         got = wl.run_loop(wl.fdtd_program(), state, 6, dtype=dtype, devices=devs)
         for g, w in zip(got.state_arrays(), want):
             assert np.array_equal(np.asarray(g, npd), w), (tj, chunks)
+    env(IB_FDTD_TJ=0, IB_FDTD_CHUNKS=0)
+    for run in (lambda: wl.run_batched(wl.fdtd_program(), state, 3, 2, dtype=dtype, devices=devs,
+                                       build="capture", halo="copy"),
+                lambda: wl.run_loop(wl.fdtd_program(), state, 6, dtype=dtype, devices=devs, halo="copy")):
+        for g, w in zip(run().state_arrays(), want):  # IB_HALO_COPY: peer-copy nodes move the halos
+            assert np.array_equal(np.asarray(g, npd), w)

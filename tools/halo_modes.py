@@ -10,12 +10,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl  # noqa: E402
 
 CASES = [("hotspot3d", [512, 8], 1000, 20), ("hotspot3d", [1024, 1024, 64], 100, 10),
-         ("hotspot3d", [2048, 2048, 64], 40, 10)]
+         ("hotspot3d", [2048, 2048, 64], 40, 10), ("fdtd", [256], 100, 20)]
 print("| grid | slabs | exchange | graph us/iter | stream us/iter |")
 print("|---|---|---|---|---|")
 for w, size, n, k in CASES:
     st = cli.build_workload(w, size)
-    shape = "x".join(map(str, st.temperature.shape))
+    shape = "x".join(map(str, st.temperature.shape)) if w != "fdtd" else "fdtd " + "x".join(map(str, st.dims))
     for slabs, halo in ((1, "store"), (2, "store"), (2, "copy"), (4, "store"), (4, "copy")):
         s = wl.DeviceSolver(st, "f32", devices=[0] * slabs if slabs > 1 else None, halo=halo)
         try:
