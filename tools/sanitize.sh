@@ -20,6 +20,7 @@ for tool in memcheck racecheck; do
   san $tool hotspot3d 30,16,8 f32 "--slabs 3"; san $tool hotspot2d 41,128 f64 "--slabs 2 --halo copy"
   KTAG=tma IB_HOTSPOT_KERNEL=tma san $tool hotspot3d 40,16,256 f32 "--slabs 2"
   san $tool fdtd 20,17,40 f32 "--slabs 3"; san $tool fdtd 20,17,40 f64 "--slabs 3 --fuse"
+  san $tool fdtd 20,17,40 f32 "--slabs 2 --halo copy"; san $tool fdtd 20,17,40 f32 "--slabs 2 --fuse --halo copy"
 done
 san synccheck hotspot2d 40,128 f32; san synccheck fdtd 20,17,40 f32 --fuse; san synccheck fdtd 20,17,40 f32
 KTAG=tma IB_HOTSPOT_KERNEL=tma san synccheck hotspot3d 40,16,256 f32
