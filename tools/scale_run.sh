@@ -19,5 +19,5 @@ for N in 1 2 4 8; do
   python -c "
 import json; d = json.loads(open('gpurun_out/scale/bench_n$N.json').readline())
 c = d['configs'].get('hotspot3d_large', {})
-print('N=$N', 'headline', d['value'], d['unit'], '| hotspot3d_large', c.get('us_per_iter'), c.get('n_ranks', ''))"
+print('N=$N', 'headline', d['value'], d['unit'], '| hotspot3d_large us/iter', c.get('us_per_iter'), 'HBM frac per GPU', c.get('roofline', {}).get('frac'))"
 done
