@@ -212,7 +212,7 @@ __device__ __forceinline__ T hotspot_cell(T up, T c, T dn, T ym, T yp, T zm, T z
 // (Hotspot2D 2.33 -> 3.6 / 2.7 us/iter).
 // Requires M = C*L divisible by V and, in 3-D, L divisible by V (a group never straddles a
 // y-row). block = (bx groups of a row, by row-blocks): 512 threads (256 x 2) for 2-D, 256 for
-// 3-D by default (launch layer). An EMPTY kernel's per-launch floor in a PDL graph falls with
+// 3-D by default, 1024 (128 x 8, R = 4) for 3-D grids whose CTAs then fit one wave (launch layer). An EMPTY kernel's per-launch floor in a PDL graph falls with
 // fewer, bigger CTAs (1024 x 256 threads 1.41 us, 256 x 1024 0.57 us, tools/microbench_floor.cu),
 // but 1024-thread CTAs measured slower here — a CTA retires at its slowest warp.
 // grid = (ceil(M/V/bx), ceil(rows/(R*by))).

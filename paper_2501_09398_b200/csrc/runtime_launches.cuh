@@ -136,9 +136,18 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         // bigger CTAs (tools/microbench_floor.cu): real CTAs retire at their slowest warp.
         // With shuffles and R = 2 (below), 2-D measured best at 512 threads (256 x 2 row-blocks:
         // 2.33 vs 2.43 us/iter at 256), 3-D at 256 (4.21; 512: 4.61).
-        int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? 256 : 512);
+        // 3-D grids of >= 2^19 groups with whole-warp rows (Hotspot3D 512^2x8): 4 rows per thread
+        // in 128 x 8-thread CTAs measured 2% faster than 2 rows in 256 x 1 (4.10 vs 4.20 us/iter,
+        // interleaved repeats, tools/hotspot3d_repeat.py; tools/cta_shape_tune.py swept the rest).
+        // Only while those 1024-thread CTAs (one per SM at <= 64 registers) fit in one wave:
+        // 768x512x8 (192 CTAs) ran 30% slower than the 256 x 1 shape.
+        const bool wide3d = d3 && threads_per_row * rows >= (1LL << 19) && threads_per_row % 32 == 0 &&
+                            32 % (L / V) == 0 &&
+                            ((threads_per_row + 127) / 128) * ((rows + 31) / 32) <= c->num_sms;
+        int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? (wide3d ? 1024 : 256) : 512);
         bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
-        const int64_t bx = std::min<int64_t>(std::min<int64_t>(256, bs), (threads_per_row + 31) / 32 * 32);
+        const int64_t bx_max = std::max<int64_t>(32, env_int("IB_HOTSPOT_BX", wide3d ? 128 : 256) / 32 * 32);  // CTA width cap
+        const int64_t bx = std::min<int64_t>(std::min<int64_t>(bx_max, bs), (threads_per_row + 31) / 32 * 32);
         const int64_t by = std::max<int64_t>(1, bs / bx);
         const int64_t xblocks = (threads_per_row + bx - 1) / bx;
         if (R <= 0) {
@@ -156,6 +165,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", 1);
         if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
         if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
+        if (wide3d && sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 4) R = 4;
         const void *fn = vec_fn<T>(d3, (int)R, (int)std::min<int64_t>(sh, 2), fsys != 0);
         dim3 grid((unsigned)xblocks, (unsigned)((rows + R * by - 1) / (R * by)));
         out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)by), g, src, dst, (const T *)s.power,
