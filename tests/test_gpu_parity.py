@@ -327,7 +327,9 @@ def test_describe_reports_the_chosen_variants(gpu):
     (h2,) = kernels("hotspot2d", [1024])
     assert h2["kernel"].startswith("_ZN2ib13k_hotspot_vec") and h2["block"] == [256, 2, 1]
     (h3,) = kernels("hotspot3d", [512, 8])
-    assert h3["kernel"].startswith("_ZN2ib13k_hotspot_vec") and h3["block"] == [256, 1, 1]
+    # R = 4 rows per thread in 128 x 8-thread CTAs, one wave (128 CTAs)
+    assert h3["kernel"].startswith("_ZN2ib13k_hotspot_vecIfLb1ELi4E") and h3["block"] == [128, 8, 1]
+    assert h3["grid"] == [8, 16, 1]
     f = kernels("fdtd", [256])
     assert len(f) == 2 and all("k_fdtd_lf" in k["kernel"] for k in f) and [k["step"] for k in f] == [0, 1]
     assert all(k["smem"] > 200 * 1024 for k in f)  # the 6-stage ring
