@@ -16,7 +16,7 @@ LIB = os.path.join(ROOT, "paper_2501_09398_b200", "libiterbatch_b200.so")
 KEYS = ["UBLKCP", "SYNCS", "ACQBULK", "PREEXIT", "SHFL", "LDG.E.128", "STG.E.128", "LDS", "STS",
         "MEMBAR", "FFMA", "DFMA", "FMUL", "DMUL"]
 # the kernels the bench configs run (f32) and their f64 twins
-WANT = [r"k_vector_f32ILb0E", r"k_hotspot_vecIfLb0ELi2ELi1ELb0E", r"k_hotspot_vecIfLb1ELi2ELi1ELb0E",
+WANT = [r"k_vector_f32ILb0E", r"k_hotspot_vecIfLb0ELi2ELi1ELb0E", r"k_hotspot_vecIfLb1ELi4ELi1ELb0E",
         r"k_hotspot_vecIfLb1ELi2ELi1ELb1E", r"k_hotspot_tmaIfLb1ELi2E", r"k_fdtd_lfIfLb1ELi4ELi1ELb0E",
         r"k_fdtd_lfIfLb1ELi4ELi2ELb0E", r"k_fdtd_lfIfLb1ELi4ELi0ELb0E", r"k_fdtd_lfIfLb1ELi4ELi3ELb0E",
         r"k_hotspot_vecIdLb0ELi2ELi1ELb0E", r"k_fdtd_lfIdLb1ELi2ELi0ELb0E", r"k_dist_wait", r"k_dist_signal"]
