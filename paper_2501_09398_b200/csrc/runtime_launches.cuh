@@ -57,7 +57,10 @@ HotKernel hotspot_variant(const ib_ctx *c, int rows) {
     if (!std::strcmp(force, "scalar")) return HotKernel::Scalar;
   }
   const int64_t state_bytes = 3 * M * c->dims[0] * (int64_t)sizeof(T);
-  if (tma_ok && state_bytes >= (96LL << 20)) return HotKernel::Tma;
+  // the state (T twice + P) against the 126 MB L2: measured crossover (tools/hotspot_vec_vs_tma.py,
+  // us/iter vec / tma): 3-D 1024^2x8 (100.7 MB) 16.3 / 19.0, 1280x1024x8 (126 MB) 22.6 / 22.5,
+  // 1536x1024x8 27.1 / 25.7; 2-D 2048^2 (50 MB) 8.3 / 8.9, 3072^2 (113 MB) 19.3 / 18.0.
+  if (tma_ok && state_bytes >= (104LL << 20)) return HotKernel::Tma;
   if (vec_ok) return HotKernel::Vec;
   return HotKernel::Scalar;
 }
