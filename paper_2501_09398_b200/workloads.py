@@ -761,7 +761,8 @@ def time_workload(program, state, plan, order, repeats: int = 10, workers: int |
 
 def time_workload_phases(program, state, plan, order, repeats: int = 10, *, dtype="f64",
                          devices=None, build: str = "manual", pdl: bool = False,
-                         while_loop: bool = False, meminfo: bool = False, fuse: bool = False) -> dict:
+                         while_loop: bool = False, meminfo: bool = False, fuse: bool = False,
+                         patch: bool = False) -> dict:
     """Per-repeat samples split into the paper's phases.
 
     Returns {"creation": [T_C...], "execution": [T_E...], "total": [...], "gpu": [device T_E...],
@@ -781,7 +782,7 @@ def time_workload_phases(program, state, plan, order, repeats: int = 10, *, dtyp
         if batched:
             t0 = time.perf_counter()
             tb = s.build_graph(plan.batch_size, build=build, pdl=pdl, while_loop=while_loop,
-                               meminfo=meminfo and r == 0)
+                               meminfo=meminfo and r == 0, patch=patch)
             te = s.run_graph(plan.num_batches)
             total = time.perf_counter() - t0
             s.destroy_graph()

@@ -40,7 +40,10 @@ def main():
     a = ap.parse_args()
     out = [f"# Performance-model fit on B200 ({a.round})", "",
            "Sweeps: `python -m paper_2501_09398_b200 sweep` (binary32, 5 repeats per K, every divisor of "
-           "I_k up to 25% of I_k, host wall-clock T_C and T_E as in the paper). Fits and the optimum are "
+           "I_k up to 25% of I_k, host wall-clock T_C and T_E as in the paper; the driver's one-time "
+           "graph-memory growth paid before the sweep; odd K on the ping-pong solvers builds ONE executable "
+           "re-pointed per launch (`IB_FLAG_PATCH`), so T_C is one K-node graph as the linear creation "
+           "model assumes). Fits and the optimum are "
            "computed by the reference's own `fit_creation`, `fit_execution` (validity filter 0.25 I_k, "
            "`fitting.py:104-134`) and `recommend_from_coefficients` (`optimize.py:135-165`), unchanged.", "",
            "| config | k_c (s/node) | b_c (s) | a (s·node) | b (s) | exec MAE (s) | K* (reference optimizer) | "
