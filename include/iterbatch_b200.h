@@ -135,7 +135,8 @@ int ib_download(ib_ctx *ctx, int field, void *host, size_t bytes);
 /* Bytes one iteration moves by the roofline convention (every array read once, written once). */
 int64_t ib_iteration_bytes(const ib_ctx *ctx);
 /* The kernels one iteration launches (the variant the runtime chose for this shape and device):
- * a JSON array of {"kernel", "grid", "block", "smem", "slab", "step"}, NUL-terminated into buf
+ * a JSON array of {"kernel", "grid", "block", "smem", "slab", "step"} (with IB_HALO_COPY each
+ * launch is followed by {"memcpy_nodes", "slab", "step"}: the peer copies after it), NUL-terminated into buf
  * (truncated to cap). Returns the full length including the NUL, or a negative status. */
 int64_t ib_describe(ib_ctx *ctx, char *buf, int64_t cap);
 

@@ -429,6 +429,15 @@ int64_t ib_describe(ib_ctx *c, char *buf, int64_t cap) {
                   i ? ", " : "", name, L.grid.x, L.grid.y, L.grid.z, L.block.x, L.block.y, L.block.z,
                   L.smem, L.slab, L.step);
     js += row;
+    if (copies_halos(c)) {  // IB_HALO_COPY: the peer copies that follow this launch
+      const int P = (int)c->slabs.size();
+      const int up = L.slab > 0, dn = L.slab + 1 < P;  // neighbours above / below
+      const int n = c->hotspot() ? up + dn
+                    : c->solver == IB_SOLVER_FDTD_FUSED ? 6 * dn + 3 * up
+                    : (L.step == 0 ? 3 * dn : 3 * up);  // H: H fields down, E: E fields up
+      std::snprintf(row, sizeof(row), ", {\"memcpy_nodes\": %d, \"slab\": %d, \"step\": %d}", n, L.slab, L.step);
+      js += row;
+    }
   }
   js += "]";
   if (buf && cap > 0) {

@@ -507,7 +507,8 @@ class DeviceSolver:
 
     def describe(self) -> list:
         """The kernel launches of one iteration as the runtime chose them for this shape:
-        [{"kernel", "grid", "block", "smem", "slab", "step"}, ...] (ib_describe)."""
+        [{"kernel", "grid", "block", "smem", "slab", "step"}, ...] (ib_describe); with
+        halo="copy", each launch is followed by {"memcpy_nodes", "slab", "step"}."""
         import json
 
         L = _lib.lib()

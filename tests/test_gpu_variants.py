@@ -110,6 +110,8 @@ def test_hotspot_slabs_copy_exchange(gpu, env, kernel, slabs):
         state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
         want = ocpu.hotspot(state.temperature, state.power, 0.1, 6, np.float64)
         with wl.DeviceSolver(state, "f64", devices=[0] * slabs, halo="copy") as s:
+            d = s.describe()  # kernels plus the peer-copy nodes after each (2 per interior slab)
+            assert sum(e.get("memcpy_nodes", 0) for e in d) == 2 * (slabs - 1)
             s.run_stream(6)
             assert np.array_equal(s.download(state).temperature, want), shape
             s.upload(state)
