@@ -169,6 +169,12 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
         if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
         if (wide3d && sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 4) R = 4;
+        // 2-D grids past one wave of the 256 x 2 / R = 2 shape (two 512-thread CTAs per SM at 49
+        // registers): one row per thread (~30 registers, four CTAs per SM) measured faster —
+        // 2048^2 7.89 vs 8.67 us/iter, 1536^2 5.92 vs 6.75 (tools/hotspot2d_shapes.py)
+        if (!d3 && sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && R == 2 &&
+            xblocks * ((rows + 2 * by - 1) / (2 * by)) > 2LL * c->num_sms)
+          R = 1;
         const void *fn = vec_fn<T>(d3, (int)R, (int)std::min<int64_t>(sh, 2), fsys != 0);
         dim3 grid((unsigned)xblocks, (unsigned)((rows + R * by - 1) / (R * by)));
         out.push_back(make_launch(fn, grid, dim3((unsigned)bx, (unsigned)by), g, src, dst, (const T *)s.power,
