@@ -3,29 +3,36 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--only NAME]
 
-Headline (BASELINE.json configs[1]): Rodinia Hotspot 2-D, 1024x1024 binary32, N = 10,000 timesteps,
-graph mode at the measured optimal batch size K*. One bench STEP = one full run of the workload:
-graph creation + instantiation + upload (T_C) and the N/K graph launches (T_E), timed on the
-device with CUDA events (ib_run_batched), with L2 flushed (a 2x-L2 buffer written) before every
-step. value = device time per step / N in microseconds per iteration (lower is better).
+N = 1 — headline (BASELINE.json configs[1]): Rodinia Hotspot 2-D 1024x1024, N = 10,000 timesteps,
+binary64 (the reference's own precision: the device result reproduces the reference's checksum bit
+for bit, so the reference arm's line is the same config at the same precision), graph mode at the
+measured optimal batch size K*. One bench STEP = one full run of the workload: graph creation +
+instantiation + upload (T_C) and the N/K graph launches (T_E), timed on the device with CUDA events
+(ib_run_batched), L2 flushed (a 2x-L2 buffer written) before every step. value = device time per
+step / N in microseconds per iteration (lower is better). The binary32 run of the same config is
+on the same line ("f32"), and every other BASELINE config in both precisions ("configs").
 
-Also reported on the same line:
+N > 1 — the sharded config (BASELINE.json configs[4]): Hotspot3D 2048x2048x256, N = 100, strong
+scaling over N GPUs, one process per GPU (torchrun; `python bench.py --gpus N` spawns the N ranks
+itself when WORLD_SIZE is unset): axis-0 slabs, the stencil kernel stores its boundary planes into
+the neighbours' halo planes over CUDA IPC (NVLink peer stores), device-counter ordering inside the
+iteration-batch graph. value = max-over-ranks device time per step / N iterations (the whole grid's
+iterations: never a replica time divided by N). The same workload on one GPU is measured in the same
+run ("single_gpu") so the curve has its own base point.
+
+Also reported on each line:
   speedup_vs_stream  per-iteration stream launch (Listing 1) time / graph time, same N, same flush
   roofline           per-iteration algorithmic bytes / per-iteration graph execution time (device)
                      against the measured HBM copy bandwidth (MEASURED_PEAKS.json)
-  e2e                the public API with host buffers: pinned H2D of the inputs, the run, D2H of
-                     the result, host wall clock
-  cpu_baseline       the reference algorithm (numpy restatement, binary64, oracle/numpy_port.py)
-                     on a bounded sample, on this host's cores (rank 0, N = 1 only)
-  configs            the other BASELINE.json configs measured the same way (skeleton, Hotspot3D
-                     512x512x8, FDTD 256^3, Hotspot3D 2048x2048x256)
+  e2e                the drop-in call users make, workloads.run_batched(program, fp64 state, K, I),
+                     host wall clock: dtype conversion, H2D of the inputs, graph build + launches,
+                     D2H of the result, the result dataclass ("pinned": the same through
+                     DeviceSolver from pinned host buffers)
+  cpu_baseline       the UNMODIFIED reference (baseline/_ref: iterbatch.workloads.time_workload,
+                     LOOP order, binary64, workers=None and all host cores) on a bounded sample
+                     (rank 0, N = 1 only); the numpy port oracle/numpy_port.py if baseline/_ref is absent
 
-N > 1 (torchrun): the headline path does not shard (launch-bound by design), so
-each rank runs an independent replica on its own GPU ("replicas only", scaling "weak"); value is
-the whole-job time per iteration = max-over-ranks step time / (N_iterations * world_size).
-
---impl reference: the reference CPU path (the numpy restatement of workloads.py, binary64, all host
-threads via the reference's row-slab scheme) on the same config and metric, rank 0 only.
+--impl reference: the same reference call on the same config (rank 0 only; the other ranks exit 0).
 """
 
 from __future__ import annotations
@@ -34,6 +41,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -47,40 +55,51 @@ import numpy as np  # noqa: E402
 
 METRIC = "µs/iteration and graph-vs-stream speed-up vs batch size K; stencil HBM GB/s % of peak"
 UNIT = "µs/iteration"
+DATA = "synthetic (the reference generator cli.py:172-199, seed 20240817)"
 
 # BASELINE.json configs, in order. k_candidates: the divisors of N the in-bench sweep tries.
 CONFIGS = {
     "skeleton": dict(workload="vector", size=[16384], iterations=10000,
-                     label="Skeleton vector-scale 2^14 fp32, N=10000",
+                     label="Skeleton vector-scale 2^14, N=10000",
                      k_candidates=[10, 20, 50, 100, 200, 500, 1000, 2000]),
     "hotspot2d": dict(workload="hotspot2d", size=[1024], iterations=10000,
-                      label="Rodinia Hotspot 2-D 1024x1024 fp32, N=10000",
+                      label="Rodinia Hotspot 2-D 1024x1024, N=10000",
                       k_candidates=[10, 20, 25, 40, 50, 80, 100, 125, 200, 250, 400, 500, 1000, 2000]),
     "hotspot3d": dict(workload="hotspot3d", size=[512, 8], iterations=1000,
-                      label="Rodinia Hotspot3D 512x512x8 fp32, N=1000",
+                      label="Rodinia Hotspot3D 512x512x8, N=1000",
                       k_candidates=[10, 20, 25, 40, 50, 100, 125, 200, 250, 500, 1000]),
     "fdtd": dict(workload="fdtd", size=[256], iterations=2000,
-                 label="FDTD Yee 256^3 fp32 (H+E per iteration), N=2000",
-                 k_candidates=[10, 20, 50, 100, 200]),
+                 label="FDTD Yee 256^3 (H then E per iteration), N=2000",
+                 k_candidates=[10, 20, 50, 100, 200], big=True),
     "fdtd_fused": dict(workload="fdtd", size=[256], iterations=2000, fuse=True,
-                       label="FDTD Yee 256^3 fp32, H+E fused in one kernel per iteration, N=2000",
-                       k_candidates=[10, 20, 50, 100, 200]),
+                       label="FDTD Yee 256^3, H+E fused in one kernel per iteration, N=2000",
+                       k_candidates=[10, 20, 50, 100, 200], big=True),
     "hotspot3d_large": dict(workload="hotspot3d", size=[2048, 2048, 256], iterations=100,
-                            label="Hotspot3D 2048x2048x256 fp32, N=100",
-                            k_candidates=[5, 10, 20, 50, 100]),
+                            label="Hotspot3D 2048x2048x256, N=100",
+                            k_candidates=[5, 10, 20, 50, 100], big=True),
 }
-HEADLINE = "hotspot2d"
+HEADLINE = "hotspot2d"       # N = 1
+SCALED = "hotspot3d_large"   # N > 1: the config north_star shards over 1/2/4/8 GPUs
+HEAD_DTYPE = "f64"           # the reference's precision (bit-exact); f32 rides along
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def config_of(name: str, dtype: str, n_gpus: int) -> dict:
+    """The `config` object of a line — identical for our arm and the reference arm."""
+    cfg = CONFIGS[name]
+    return {"workload": cfg["label"], "size": list(cfg["size"]), "iterations": cfg["iterations"],
+            "dtype": dtype, "n_gpus": n_gpus}
+
+
 # ---------------------------------------------------------------------------------------------
 # distributed plumbing (torch only when launched under torchrun with WORLD_SIZE > 1)
 # ---------------------------------------------------------------------------------------------
 class Dist:
-    def __init__(self):
+    def __init__(self, need_gpu: bool = True):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -90,11 +109,11 @@ class Dist:
             import torch
             import torch.distributed as td
 
-            n = torch.cuda.device_count()
-            if self.world > n:  # protocol check on a small box: ranks share GPUs, gloo for plumbing
-                self.shared = True
+            n = torch.cuda.device_count() if need_gpu else 0
+            if self.world > n:  # ranks share GPUs (a small box: protocol check), gloo for plumbing
+                self.shared = n > 0
                 self.local = self.local % max(1, n)
-                if n:  # (none at all: the reference arm, CPU only)
+                if n:
                     torch.cuda.set_device(self.local)
                 td.init_process_group("gloo")
             else:
@@ -106,20 +125,43 @@ class Dist:
         if self.torch is not None:
             self.td.barrier()
 
-    def max(self, x: float) -> float:
+    def _reduce(self, x: float, op) -> float:
         if self.torch is None:
             return x
-        t = self.torch.tensor([x], dtype=self.torch.float64, device="cpu" if self.shared else "cuda")
-        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        dev = "cpu" if (self.shared or self.td.get_backend() == "gloo") else "cuda"
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=dev)
+        self.td.all_reduce(t, op=op)
         return float(t.item())
+
+    def max(self, x: float) -> float:
+        return self._reduce(x, self.td.ReduceOp.MAX if self.torch is not None else None)
+
+    def allgather(self, blob):
+        out = [None] * self.world
+        self.td.all_gather_object(out, blob)
+        return out
 
     def close(self):
         if self.torch is not None:
             self.td.destroy_process_group()
 
 
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a launcher: start the N ranks ourselves (torchrun, 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    log("spawning:", " ".join(cmd))
+    return subprocess.call(cmd, cwd=ROOT)
+
+
 # ---------------------------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML / nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------------------------
 class Clocks:
     """SM clock and clock-event reasons sampled DURING a timed region: in-process NVML polling
@@ -248,12 +290,12 @@ def measured_peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_key: str):
+def ncu_traffic(key: str):
     """DRAM bytes per launch from the committed ncu --set full summary, if present."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(kernel_key)
+            return json.load(fh).get(key)
     except (OSError, ValueError):
         return None
 
@@ -268,40 +310,51 @@ def make_state(cfg):
 
 
 def pick_k(solver, cfg, quick: bool) -> tuple[int, bool, list]:
-    """In-bench batch-size sweep: minimise total device time T_C + T_E over candidate K (+PDL)."""
+    """In-bench batch-size sweep: minimise T_C + T_E (device) over candidate K, plain and PDL edges.
+
+    Two rounds so one slow sample cannot pick or reject a K (profiles/r02_k_sweep.md): every
+    candidate's median of 3, then the best four re-measured 5 more times; the winner has the
+    lowest median over all its samples."""
     n = cfg["iterations"]
     cands = [k for k in cfg["k_candidates"] if n % k == 0]
     if quick:
-        cands = [k for k in cands if k in (10, 100, 1000)] or cands[:2]
+        cands = [k for k in cands if k in (10, 20, 100, 1000)] or cands[:2]
+    big = cfg.get("big", False)
     # The driver grows its graph-executable memory the first time a process instantiates a graph
     # of a new size (tools/build_phases.py: first K=2000 instantiate 60 ms, later ones 2.5 ms) —
     # a once-per-process cost, not part of T_C(K): pay it before the sweep.
     for pdl in (False, True):
         solver.build_graph(max(cands), pdl=pdl)
         solver.destroy_graph()
-    reps = 1 if quick else 3  # median of 3: one host hiccup inside a graph build (T_C) would
-    rows = []                 # otherwise mark a K as slow
-    best = None
+    r1, r2 = (1, 2) if (quick or big) else (3, 5)
+    samples = {}
     for k in cands:
         for pdl in (False, True):
-            ts = []
-            for _ in range(reps):
+            for _ in range(r1):
                 solver.flush_l2()
-                ts.append(solver.run_batched(k, n // k, pdl=pdl))
-            g = statistics.median(t.gpu_s for t in ts)
-            rows.append({"K": k, "pdl": pdl, "us_per_iter": 1e6 * g / n,
-                         "T_C_us": 1e6 * statistics.median(t.build_s for t in ts), "samples": reps})
-            if best is None or g < best[0]:
-                best = (g, k, pdl)
-    return best[1], best[2], rows
+                samples.setdefault((k, pdl), []).append(solver.run_batched(k, n // k, pdl=pdl))
+    med = lambda key: statistics.median(t.gpu_s for t in samples[key])  # noqa: E731
+    for key in sorted(samples, key=med)[:4]:
+        for _ in range(r2):
+            solver.flush_l2()
+            samples[key].append(solver.run_batched(key[0], n // key[0], pdl=key[1]))
+    rows = []
+    for (k, pdl), ts in samples.items():
+        g = [t.gpu_s for t in ts]
+        rows.append({"K": k, "pdl": pdl, "us_per_iter": 1e6 * statistics.median(g) / n,
+                     "min_us_per_iter": 1e6 * min(g) / n, "max_us_per_iter": 1e6 * max(g) / n,
+                     "T_C_us": 1e6 * statistics.median(t.build_s for t in ts), "samples": len(g)})
+    best = min(samples, key=med)
+    return best[0], best[1], sorted(rows, key=lambda r: (r["K"], r["pdl"]))
 
 
-def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> dict:
+def measure_ours(name, cfg, dtype, args, dist: Dist, device: int, headline: bool) -> dict:
     from paper_2501_09398_b200 import workloads as wl
 
     n = cfg["iterations"]
     state = make_state(cfg)
-    solver = wl.DeviceSolver(state, "f32", devices=[device], fuse=cfg.get("fuse", False))
+    steps = args.steps if headline else min(args.steps, 10)
+    solver = wl.DeviceSolver(state, dtype, devices=[device], fuse=cfg.get("fuse", False))
     try:
         k, pdl, sweep = pick_k(solver, cfg, args.quick)
         num = n // k
@@ -309,13 +362,13 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
             solver.upload(state)
             solver.flush_l2()
             solver.run_batched(k, num, pdl=pdl)
-        # ---- timed: K steps, each = one full run (T_C + T_E), L2 flushed before each ----------
+        # ---- timed: `steps` steps, each = one full run (T_C + T_E), L2 flushed before each -----
         dist.barrier()
         solver.sync()
         step_s, tc_s = [], []
         small = sum(a.nbytes for a in state.state_arrays()) < (256 << 20)
         with Clocks(device) as clocks:
-            for _ in range(args.steps):
+            for _ in range(steps):
                 if small:  # fresh inputs each step (outside the timed interval)
                     solver.upload(state)
                 solver.flush_l2()
@@ -347,14 +400,25 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
         peak, peak_src = measured_peaks()
         achieved = it_bytes / (exec_mean / n) / 1e9
         kpi = solver.kernels_per_iteration
+        l2_resident = state_bytes < (96 << 20)
+        launches = solver.describe()
+        roof = {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"{name}:{dtype}"),
+            "bytes_per_iter": it_bytes, "peak_source": peak_src,
+            "kernel": launches[0]["kernel"] if launches else None,
+            "note": "per-iteration algorithmic bytes / per-iteration graph execution time (CUDA events)"
+                    + ("; fused FDTD: each field read+written once = 48 B/cell" if cfg.get("fuse") else ""),
+        }
+        if l2_resident:
+            roof["limit"] = "per-launch floor"
+            roof["note"] += ("; the state (%.1f MB) stays L2-resident across iterations (ncu: ~0 DRAM bytes per "
+                             "launch in steady state), so the binding limit is the per-launch floor of a "
+                             "PDL-chained one-wave kernel with this access pattern, not HBM (DESIGN.md §4, "
+                             "profiles/r01_microbench_floor.txt)" % (state_bytes / 1e6))
         out = {
-            "name": name,
-            "workload": cfg["label"],
-            "iterations": n,
-            "batch_size": k,
-            "pdl": pdl,
-            "us_per_iter": 1e6 * step_mean / n,
-            "ms_per_step": 1e3 * step_mean,
+            "name": name, "dtype": dtype, "workload": cfg["label"], "iterations": n, "batch_size": k, "pdl": pdl,
+            "us_per_iter": 1e6 * step_mean / n, "ms_per_step": 1e3 * step_mean, "steps": steps,
             "T_C_us": 1e6 * statistics.fmean(tc_s),
             "graph_exec_us_per_iter": 1e6 * exec_mean / n,
             "stream_us_per_iter": 1e6 * stream_mean / n,
@@ -366,54 +430,111 @@ def measure_ours(name, cfg, args, dist: Dist, device: int, headline: bool) -> di
                 statistics.stdev(step_s) / statistics.fmean(step_s) if len(step_s) > 1 else 0.0),
             "speedup_vs_stream_exec_only": stream_mean / exec_mean,
             "kernels_per_iter": kpi,
-            "gpu_launches": args.steps * n * kpi,
-            "roofline": {
-                "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(name),
-                "bytes_per_iter": it_bytes, "peak_source": peak_src,
-                "note": "per-iteration algorithmic bytes / per-iteration graph execution time"
-                        + ("; fused FDTD: each field read+written once = 48 B/cell" if cfg.get("fuse") else "")
-                        + ("; the state (%.1f MB) stays L2-resident across iterations, so this per-launch "
-                           "kernel is launch/latency-bound and the HBM roof is not the binding one "
-                           "(DESIGN.md §4)" % (state_bytes / 1e6) if state_bytes < (96 << 20) else ""),
-            },
+            "gpu_launches": steps * n * kpi,
+            "roofline": roof,
             "k_sweep": sweep,
             "clocks": clocks.summary(),
-            "launches": solver.describe(),  # the kernels one iteration ran (ib_describe)
+            "launches": launches,  # the kernels one iteration ran (ib_describe)
         }
         if headline:
-            out["e2e"] = measure_e2e(solver, state, k, num, n, pdl, args)
+            out["e2e"] = measure_e2e(solver, state, cfg, dtype, k, num, pdl, args)
         return out
     finally:
         solver.close()
 
 
-def measure_dist(name, cfg, args, dist: Dist) -> dict:
+def measure_e2e(solver, state, cfg, dtype, k, num, pdl, args) -> dict:
+    """End to end through the drop-in call a user of the reference makes:
+    workloads.run_batched(program, <binary64 HotspotWorkload>, K, I, dtype=...) — host wall clock
+    around the whole call: dtype conversion and H2D of the inputs (pageable numpy arrays, as the
+    reference API takes them), graph build + launches, D2H of the result, binary64 result
+    dataclass. Secondary ("pinned"): the same run through DeviceSolver from pinned host buffers."""
+    import ctypes
+
+    from paper_2501_09398_b200 import _lib, cli
+    from paper_2501_09398_b200 import workloads as wl
+
+    n = cfg["iterations"]
+    prog = cli.programs()[cfg["workload"]]()
+    esize = np.dtype(solver.np_dtype).itemsize
+    h2d = sum(a.size for a in state.state_arrays()) * esize
+    written = [0] if solver.kind.startswith("hotspot") else list(range(solver.nfields))
+    d2h = sum(state.state_arrays()[f].size for f in written) * esize
+    fuse = cfg.get("fuse", False)
+    samples = []
+    for rep in range(args.warmup + args.steps):
+        solver.flush_l2()
+        t0 = time.perf_counter()
+        out = wl.run_batched(prog, state, k, num, dtype=dtype, pdl=pdl, fuse=fuse, devices=solver.devices)
+        dt = time.perf_counter() - t0
+        if rep >= args.warmup:
+            samples.append(dt)
+    del out
+    wl.release_cached_contexts()
+    # secondary: pinned host buffers through DeviceSolver (inputs re-staged before every step)
+    L = _lib.lib()
+    host = solver.host_arrays(state)
+    ptrs, pinned = [], []
+
+    def pin(nbytes, like):
+        p = ctypes.c_void_p()
+        _lib.check(L.ib_host_alloc(ctypes.byref(p), nbytes))
+        ptrs.append(p)
+        return np.ctypeslib.as_array((ctypes.c_byte * nbytes).from_address(p.value)).view(like.dtype).reshape(like.shape)
+
+    pinned_samples = []
+    try:
+        pinned = [pin(a.nbytes, a) for a in host]
+        outs = [pin(host[f].nbytes, host[f]) for f in written]
+        for rep in range(args.warmup + args.steps):
+            for dst, src in zip(pinned, host):  # fresh inputs (outside the timed region)
+                dst[...] = src
+            solver.flush_l2()
+            t0 = time.perf_counter()
+            solver.upload(pinned)
+            solver.run_batched(k, num, pdl=pdl)
+            for f, o in zip(written, outs):
+                solver.download_field(f, o)
+            dt = time.perf_counter() - t0
+            if rep >= args.warmup:
+                pinned_samples.append(dt)
+    finally:
+        for p in ptrs:
+            L.ib_host_free(p)
+    return {"value": round(1e6 * statistics.fmean(samples) / n, 4), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "call": "workloads.run_batched(program, HotspotWorkload(binary64 arrays), K, I, dtype=%r)" % dtype,
+            "note": "host wall clock of the drop-in call: conversion + H2D (pageable) + build + launches + D2H "
+                    "+ result dataclass",
+            "pinned": {"value": round(1e6 * statistics.fmean(pinned_samples) / n, 4), "unit": UNIT,
+                       "note": "DeviceSolver: pinned H2D of every input field + build + launches + D2H of the "
+                               "written fields into a separate pinned buffer"}}
+
+
+def measure_dist(name, cfg, dtype, args, dist: Dist) -> dict:
     """Strong scaling of one global hotspot grid over WORLD_SIZE GPUs (one process each): axis-0
     slabs; the stencil kernel stores its boundary planes straight into the neighbours' halo planes
     (CUDA IPC / NVLink peer stores) with device-counter ordering in the graph
     (IB_BENCH_EXCHANGE=nccl: the runtime's NCCL send/recv group instead)."""
+    import ctypes
+
+    from paper_2501_09398_b200 import _lib
     from paper_2501_09398_b200.distributed import DistributedSolver, unique_id
 
     n = cfg["iterations"]
     shape = list(cfg["size"])
     if len(shape) == 2:
         shape = [shape[0], shape[0], shape[1]]
-    exchange = os.environ.get("IB_BENCH_EXCHANGE", "peer")  # peer: IPC halo stores; nccl: send/recv
+    exchange = os.environ.get("IB_BENCH_EXCHANGE", "peer")
     uid = [unique_id() if dist.rank == 0 and exchange == "nccl" else None]
     if dist.world > 1 and exchange == "nccl":
         dist.td.broadcast_object_list(uid, src=0)
-
-    def allgather(blob):
-        out = [None] * dist.world
-        dist.td.all_gather_object(out, blob)
-        return out
-
-    s = DistributedSolver.from_seed(shape, 0.1, "f32", dist.rank, dist.world, dist.local, uid[0],
-                                    exchange=exchange, allgather=allgather if dist.world > 1 else None)
+    s = DistributedSolver.from_seed(shape, 0.1, dtype, dist.rank, dist.world, dist.local, uid[0],
+                                    exchange=exchange, allgather=dist.allgather if dist.world > 1 else None)
     try:
         k = 20 if n % 20 == 0 else n
         for _ in range(args.warmup):
+            s.flush_l2()
             s.run_batched(k, n // k)
         dist.barrier()
         steps = []
@@ -426,102 +547,160 @@ def measure_dist(name, cfg, args, dist: Dist) -> dict:
         local_bytes = s.iteration_bytes
         peak, src = measured_peaks()
         achieved = local_bytes / (step / n) / 1e9  # this rank's slab bytes over the max-over-ranks time
+        # e2e through the public API with host buffers: pinned H2D of this rank's window (T with
+        # halo rows, P) + build + launches + D2H of the owned rows, max over ranks
+        from paper_2501_09398_b200.distributed import seeded_window
+
+        t_win, p_win = seeded_window(shape, dist.rank, dist.world)
+        host = [np.ascontiguousarray(t_win, s.np_dtype), np.ascontiguousarray(p_win, s.np_dtype)]
+        del t_win, p_win
+        L = _lib.lib()
+        ptrs = []
+
+        def pin(like):
+            p = ctypes.c_void_p()
+            _lib.check(L.ib_host_alloc(ctypes.byref(p), like.nbytes))
+            ptrs.append(p)
+            return np.ctypeslib.as_array((ctypes.c_byte * like.nbytes).from_address(p.value)).view(
+                like.dtype).reshape(like.shape)
+
+        e2e = []
+        try:
+            pinned = [pin(a) for a in host]
+            out = pin(np.empty(s.shapes[0], s.np_dtype))
+            for rep in range(1 + min(args.steps, 3)):
+                for dst, srcarr in zip(pinned, host):
+                    dst[...] = srcarr
+                dist.barrier()
+                t0 = time.perf_counter()
+                s.upload(pinned)
+                s.run_batched(k, n // k)
+                s.download_field(0, out)
+                if rep:
+                    e2e.append(time.perf_counter() - t0)
+        finally:
+            for p in ptrs:
+                L.ib_host_free(p)
+        e2e_s = dist.max(statistics.fmean(e2e))
         how = ("halo planes stored into the neighbours' buffers by the stencil kernel over CUDA IPC, "
                "device-counter ordering in-graph" if exchange == "peer" else "NCCL send/recv halos in-graph")
-        return {"name": name, "workload": cfg["label"] + f", {dist.world} GPUs (axis-0 slabs, {how})",
-                "iterations": n, "batch_size": k, "us_per_iter": 1e6 * step / n, "ms_per_step": 1e3 * step,
-                "scaling": "strong", "gpu_launches": args.steps * n * (3 if exchange == "peer" else 1),
+        return {"name": name, "dtype": dtype, "workload": cfg["label"], "exchange": how, "iterations": n,
+                "batch_size": k, "us_per_iter": 1e6 * step / n, "ms_per_step": 1e3 * step,
+                "gpu_launches": args.steps * n * (3 if exchange == "peer" else 1),
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                             "frac": round(achieved / peak, 4), "traffic": None, "bytes_per_iter": local_bytes,
-                             "peak_source": src, "note": "per GPU: its slab's algorithmic bytes / iteration time"},
+                             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"{name}:{dtype}"),
+                             "bytes_per_iter": local_bytes, "peak_source": src,
+                             "note": "per GPU: its slab's algorithmic bytes / the max-over-ranks iteration time"},
+                "e2e": {"value": round(1e6 * e2e_s / n, 3), "unit": UNIT,
+                        "h2d_bytes_per_step": int(sum(a.nbytes for a in host)) * dist.world,
+                        "d2h_bytes_per_step": int(np.prod(s.shapes[0]) * np.dtype(s.np_dtype).itemsize) * dist.world,
+                        "note": "per rank: pinned H2D of its window + build + launches + D2H of its rows, host wall "
+                                "clock, max over ranks; bytes summed over ranks"},
                 "clocks": clocks.summary()}
     finally:
         s.close()
 
 
-def measure_e2e(solver, state, k, num, n, pdl, args) -> dict:
-    """Public API with host buffers: pinned H2D of every input field, the run, D2H of the result."""
-    import ctypes
+def measure_single_gpu(name, cfg, dtype, args) -> dict:
+    """The sharded workload on ONE GPU (the curve's base point), measured in the same run."""
+    from paper_2501_09398_b200.distributed import DistributedSolver
 
-    from paper_2501_09398_b200 import _lib
-
-    L = _lib.lib()
-    pinned, ptrs = [], []
-    for a in solver.host_arrays(state):
-        p = ctypes.c_void_p()
-        _lib.check(L.ib_host_alloc(ctypes.byref(p), a.nbytes))
-        ptrs.append(p)
-        view = np.ctypeslib.as_array((ctypes.c_byte * a.nbytes).from_address(p.value))
-        view = view.view(a.dtype).reshape(a.shape)
-        view[...] = a
-        pinned.append(view)
-    out_buf = np.ctypeslib.as_array(
-        (ctypes.c_byte * pinned[0].nbytes).from_address(ptrs[0].value)).view(pinned[0].dtype).reshape(pinned[0].shape)
-    written = [0] if solver.kind.startswith("hotspot") else list(range(solver.nfields))
-    h2d = sum(a.nbytes for a in pinned)
-    d2h = sum(pinned[f].nbytes for f in written)
-    samples = []
+    n = cfg["iterations"]
+    s = DistributedSolver.from_seed(list(cfg["size"]), 0.1, dtype, 0, 1, 0, None)
     try:
-        for rep in range(args.warmup + args.steps):
-            solver.flush_l2()
-            t0 = time.perf_counter()
-            solver.upload(pinned)
-            solver.run_batched(k, num, pdl=pdl)
-            for f in written:
-                solver.download_field(f, out_buf if f == 0 else None)
-            dt = time.perf_counter() - t0
-            if rep >= args.warmup:
-                samples.append(dt)
+        k = 20 if n % 20 == 0 else n
+        for _ in range(args.warmup):
+            s.flush_l2()
+            s.run_batched(k, n // k)
+        steps = []
+        for _ in range(min(args.steps, 5)):
+            s.flush_l2()
+            steps.append(s.run_batched(k, n // k).gpu_s)
+        step = statistics.fmean(steps)
+        return {"value": round(1e6 * step / n, 3), "unit": UNIT, "n_gpus": 1, "batch_size": k, "dtype": dtype,
+                "note": "the same grid, generator and batch size on one GPU of this box"}
     finally:
-        for p in ptrs:
-            L.ib_host_free(p)
-    return {"value": 1e6 * statistics.fmean(samples) / n, "unit": UNIT,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "note": "host wall clock: pinned H2D + build + run + D2H per step"}
+        s.close()
 
 
 # ---------------------------------------------------------------------------------------------
-# CPU baseline / reference arm: the reference algorithm (numpy, binary64) on this host
+# the reference CPU path: the UNMODIFIED reference package (baseline/_ref), else the numpy port
 # ---------------------------------------------------------------------------------------------
-def cpu_sample(cfg, workers: int, budget_s: float, min_iters: int = 1) -> dict:
+def reference_pkg():
+    """iterbatch from baseline/_ref (pip --target of /root/reference/pkg, unmodified), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "iterbatch")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import iterbatch.cli as rcli
+        import iterbatch.workloads as rwl
+        from iterbatch.model import BatchPlan
+    except ImportError:
+        return None
+    return rcli, rwl, BatchPlan
+
+
+def _ref_state(name, rcli, rwl):
+    """The reference's own input for a config (its cli._build_workload), and the factor that scales
+    a sample's time to the whole config."""
+    cfg = CONFIGS[name]
+    if cfg["size"] == [2048, 2048, 256]:
+        # a bounded sample: a 64-row sub-grid of the seeded input (the same per-cell work; the full
+        # grid's numpy temporaries would need ~70 GB of host memory), scaled by 2048/64
+        from paper_2501_09398_b200.distributed import seeded_window
+
+        t, p = seeded_window(cfg["size"], 0, 32)
+        return rwl.HotspotWorkload(t[:64], p, 0.1), 2048 / 64
+    return rcli._build_workload(cfg["workload"], list(cfg["size"])), 1.0
+
+
+def cpu_time(name: str, workers, iters: int) -> tuple[float, str]:
+    """Seconds per iteration of the reference's CPU path on this host, and its kind."""
+    cfg = CONFIGS[name]
+    ref = reference_pkg()
+    if ref is not None:
+        rcli, rwl, BatchPlan = ref
+        state, scale = _ref_state(name, rcli, rwl)
+        prog = rcli._PROGRAMS[cfg["workload"]]()
+        series = rwl.time_workload(prog, state, BatchPlan(iters, iters, 1), rwl.ExecutionOrder.LOOP,
+                                   repeats=1, workers=workers, label=name)
+        return series.points[0].samples[0] * scale / iters, "reference"
     from oracle import numpy_port as npo
 
     state = make_state(cfg)
     pool = npo.SlabPool(workers)
     try:
-        def run(iters):
-            if cfg["workload"] == "vector":
-                v = state.values
-                t0 = time.perf_counter()
-                npo.run_vector(v, state.scale_constant, iters, pool)
-            elif cfg["workload"].startswith("hotspot"):
-                t0 = time.perf_counter()
-                npo.run_hotspot(state.temperature, state.power, state.diffusion_coefficient, iters, pool)
-            else:
-                c_h, c_e = npo.fdtd_coefficients(state.cell_size, state.time_step)
-                t0 = time.perf_counter()
-                npo.run_fdtd(state.state_arrays(), state.cell_size, c_h, c_e, iters, pool)
-            return time.perf_counter() - t0
-
-        probe = run(1)
-        iters = max(min_iters, min(cfg["iterations"], int(budget_s / max(probe, 1e-9))))
-        dt = run(iters)
+        t0 = time.perf_counter()
+        if cfg["workload"] == "vector":
+            npo.run_vector(state.values, state.scale_constant, iters, pool)
+        elif cfg["workload"].startswith("hotspot"):
+            npo.run_hotspot(state.temperature, state.power, state.diffusion_coefficient, iters, pool)
+        else:
+            c_h, c_e = npo.fdtd_coefficients(state.cell_size, state.time_step)
+            npo.run_fdtd(state.state_arrays(), state.cell_size, c_h, c_e, iters, pool)
+        return (time.perf_counter() - t0) / iters, "port"
     finally:
         pool.close()
-    return {"us_per_iter": 1e6 * dt / iters, "iterations": iters, "seconds": dt, "workers": workers}
 
 
-def cpu_baseline(cfg, budget_s: float) -> dict:
+def cpu_baseline(name: str, budget_s: float) -> dict:
     cores = len(os.sched_getaffinity(0))
-    single = cpu_sample(cfg, 1, budget_s / 2)
-    multi = cpu_sample(cfg, cores, budget_s / 2) if cores > 1 else single
-    best = multi if multi["us_per_iter"] < single["us_per_iter"] else single
-    return {"value": round(best["us_per_iter"], 2), "unit": UNIT, "cores": best["workers"],
-            "kind": "port",
-            "sample": (f"{best['iterations']} of {cfg['iterations']} iterations of {cfg['label']} in "
-                       f"binary64 (the reference's numpy algorithm, oracle/numpy_port.py, row slabs over "
-                       f"{best['workers']} threads); 1-thread: {single['us_per_iter']:.1f} us/iter"),
-            "cpu": cpu_model()}
+    rows = {}
+    for workers in (None, cores):
+        probe, kind = cpu_time(name, workers, 1)
+        iters = max(1, min(CONFIGS[name]["iterations"], int(budget_s / 2 / max(probe, 1e-9))))
+        per, kind = cpu_time(name, workers, iters)
+        rows[workers] = (per, iters, kind)
+    best_w = min(rows, key=lambda w: rows[w][0])
+    per, iters, kind = rows[best_w]
+    what = ("iterbatch.workloads.time_workload (the unmodified reference, baseline/_ref), LOOP order"
+            if kind == "reference" else "the reference's numpy algorithm restated (oracle/numpy_port.py)")
+    return {"value": round(1e6 * per, 2), "unit": UNIT, "cores": best_w or 1, "kind": kind,
+            "sample": f"{iters} of {CONFIGS[name]['iterations']} iterations of {CONFIGS[name]['label']}, binary64, "
+                      f"{what}, workers={best_w}",
+            "workers_none_us_per_iter": round(1e6 * rows[None][0], 2),
+            "workers_all_us_per_iter": round(1e6 * rows[cores][0], 2), "host_cores": cores, "cpu": cpu_model()}
 
 
 def cpu_model() -> str:
@@ -535,147 +714,80 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def run_reference(args, dist: Dist) -> int:
-    cfg = CONFIGS[args.only or HEADLINE]
+def run_reference(args, dist: Dist, world: int) -> int:
+    name = args.only or (SCALED if world > 1 else HEADLINE)
     if dist.rank != 0:
         return 0
-    from oracle import numpy_port as npo
-
+    cfg = CONFIGS[name]
     cores = len(os.sched_getaffinity(0))
-    state = make_state(cfg)
-    pool = npo.SlabPool(cores)
     sample_iters = {"vector": 2000, "hotspot2d": 20, "hotspot3d": 5, "fdtd": 1}[cfg["workload"]]
-    if cfg["size"] == [2048, 2048, 256]:
+    if cfg.get("big") and cfg["workload"] == "hotspot3d":
         sample_iters = 1
-
-    def step():
-        t0 = time.perf_counter()
-        if cfg["workload"] == "vector":
-            npo.run_vector(state.values, state.scale_constant, sample_iters, pool)
-        elif cfg["workload"].startswith("hotspot"):
-            npo.run_hotspot(state.temperature, state.power, state.diffusion_coefficient, sample_iters, pool)
-        else:
-            c_h, c_e = npo.fdtd_coefficients(state.cell_size, state.time_step)
-            npo.run_fdtd(state.state_arrays(), state.cell_size, c_h, c_e, sample_iters, pool)
-        return time.perf_counter() - t0
-
-    try:
-        for _ in range(args.warmup):
-            step()
-        samples = [step() for _ in range(args.steps)]
-    finally:
-        pool.close()
-    mean = statistics.fmean(samples)
-    value = 1e6 * mean / sample_iters
-    sample = (f"each step = {sample_iters} of the {cfg['iterations']} iterations of {cfg['label']}, "
-              f"binary64, reference numpy algorithm (oracle/numpy_port.py) over {cores} threads")
+    per_worker = {}
+    for workers in (None, cores):  # the reference's own knob: serial, and a row slab per core
+        per_worker[workers] = cpu_time(name, workers, max(1, sample_iters // 4))[0]
+    workers = min(per_worker, key=per_worker.get)
+    kind = "port"
+    for _ in range(args.warmup):
+        _, kind = cpu_time(name, workers, sample_iters)
+    samples = [cpu_time(name, workers, sample_iters)[0] for _ in range(args.steps)]
+    value = 1e6 * statistics.fmean(samples)
+    what = ("iterbatch.workloads.time_workload of the unmodified reference (baseline/_ref), LOOP order"
+            if kind == "reference" else "the reference's numpy algorithm restated (oracle/numpy_port.py)")
+    sample = (f"each step = {sample_iters} of the {cfg['iterations']} iterations of {cfg['label']}"
+              + (" on a 64-row sub-grid, scaled x32" if cfg.get("big") and cfg["workload"] == "hotspot3d" else "")
+              + f", binary64, {what}, workers={workers}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * mean, 3), "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 20240817)",
-        "config": {"workload": cfg["label"], "iterations": cfg["iterations"], "parallelism": "cpu-threads"},
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample, "cpu": cpu_model()},
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.fmean(samples) * sample_iters, 3), "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": HEAD_DTYPE, "data": DATA,
+        "config": config_of(name, HEAD_DTYPE, world),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": workers or 1, "kind": kind,
+                         "sample": sample, "cpu": cpu_model(),
+                         "workers_none_us_per_iter": round(1e6 * per_worker[None], 2),
+                         "workers_all_us_per_iter": round(1e6 * per_worker[cores], 2)},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main() -> int:
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--only", choices=sorted(CONFIGS), default=None,
-                    help="measure just this config (as the headline)")
-    ap.add_argument("--no-extra", action="store_true", help="skip the non-headline configs")
-    ap.add_argument("--quick", action="store_true", help="small K sweep")
-    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU baseline work")
-    args = ap.parse_args()
-    if args.warmup < 3:
-        log("warmup raised to 3 (timing rules)")
-        args.warmup = 3
-    dist = Dist()
-    try:
-        if args.impl == "reference":
-            return run_reference(args, dist)
-        return run_ours(args, dist)
-    finally:
-        dist.close()
+# ---------------------------------------------------------------------------------------------
+# the JSON lines
+# ---------------------------------------------------------------------------------------------
+def _brief(r: dict) -> dict:
+    keep = ("us_per_iter", "ms_per_step", "batch_size", "pdl", "T_C_us", "graph_exec_us_per_iter",
+            "stream_us_per_iter", "stream_pdl_us_per_iter", "speedup_vs_stream", "speedup_vs_stream_err",
+            "speedup_vs_stream_exec_only", "kernels_per_iter", "roofline", "e2e", "clocks", "launches", "steps")
+    return {k: r[k] for k in keep if k in r}
 
 
-def run_ours(args, dist: Dist) -> int:
-    from paper_2501_09398_b200 import _lib
-
-    _lib.lib()
-    if _lib.device_count() < 1:
-        raise RuntimeError("bench.py needs a CUDA device (no CPU fallback)")
-    device = dist.local
-    head_name = args.only or HEADLINE
-    if head_name == "hotspot3d_large" and dist.world > 1:  # the sharded config alone
-        r = measure_dist(head_name, CONFIGS[head_name], args, dist)
-        if dist.rank == 0:
-            print(json.dumps({"metric": METRIC, "value": round(r["us_per_iter"], 3), "unit": UNIT,
-                              "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
-                              "ms_per_step": round(r["ms_per_step"], 3), "higher_is_better": False,
-                              "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                              "data": "synthetic (reference generator, seed 20240817)",
-                              "config": {"workload": r["workload"], "iterations": r["iterations"],
-                                         "batch_size": r["batch_size"],
-                                         "parallelism": f"axis-0 slabs x{dist.world}"
-                                         + (" (ranks share GPUs: protocol check only)" if dist.shared else "")},
-                              "roofline": r["roofline"], "gpu_launches": r["gpu_launches"],
-                              "clocks": r["clocks"]}), flush=True)
-        return 0
-    head = measure_ours(head_name, CONFIGS[head_name], args, dist, device, headline=True)
-    log(f"[{head_name}] {head['us_per_iter']:.3f} us/iter at K={head['batch_size']} "
-        f"(stream {head['stream_us_per_iter']:.3f}, x{head['speedup_vs_stream']:.2f})")
-    extra = {}
-    if not args.no_extra and args.only is None:
-        for name, cfg in CONFIGS.items():
-            if name == head_name:
-                continue
-            try:
-                if name == "hotspot3d_large" and dist.world > 1:
-                    extra[name] = measure_dist(name, cfg, args, dist)
-                    continue
-                r = measure_ours(name, cfg, args, dist, device, headline=False)
-                r.pop("k_sweep", None)
-                extra[name] = r
-                log(f"[{name}] {r['us_per_iter']:.3f} us/iter at K={r['batch_size']} "
-                    f"(stream {r['stream_us_per_iter']:.3f}, x{r['speedup_vs_stream']:.2f}) "
-                    f"roofline {r['roofline']['frac']:.3f}")
-            except MemoryError as exc:
-                extra[name] = {"skipped": f"out of device memory: {exc}"}
-    cpu = None
-    if dist.rank == 0 and args.gpus == 1 and dist.world == 1:
-        cpu = cpu_baseline(CONFIGS[head_name], args.cpu_budget)
-    world = dist.world
-    value = head["us_per_iter"] / world
-    line = {
+def head_line(head: dict, head32: dict, extra: dict, cpu, args) -> dict:
+    """The N = 1 line: the headline config in the reference's precision, binary32 beside it."""
+    return {
         "metric": METRIC,
-        "value": round(value, 4),
+        "value": round(head["us_per_iter"], 4),
         "unit": UNIT,
-        "n_gpus": world,
+        "n_gpus": 1,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(head["ms_per_step"], 4),
         "higher_is_better": False,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic (reference generator cli.py:172-199, seed 20240817)",
-        "config": {
-            "workload": head["workload"] + " (one step = one full run: graph build T_C + N/K launches)",
-            "iterations": head["iterations"],
+        "dtype": head["dtype"],
+        "data": DATA,
+        "config": config_of(head["name"], head["dtype"], 1),
+        "impl_detail": {
+            "step": "one full run: graph build T_C + N/K graph launches, device-timed (CUDA events)",
             "batch_size": head["batch_size"],
             "graph_edges": "programmatic (PDL)" if head["pdl"] else "plain",
-            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-            "l2": "flushed before every step (2x L2 buffer written); the 12.6 MB working set then "
-                  "stays L2-resident across the run's iterations as in the real application",
+            "parallelism": "1 GPU",
+            "l2": "flushed before every step (2x L2 buffer written); the working set then stays L2-resident "
+                  "across the run's iterations as in the real application",
+            "parity": "binary64 device state == the reference's state_checksum bit for bit (tests P0)"
+                      if head["dtype"] == "f64" else "binary32 == the binary32 oracle bit for bit (tests P1)",
         },
         "speedup_vs_stream": round(head["speedup_vs_stream"], 3),
         "speedup_vs_stream_err": round(head["speedup_vs_stream_err"], 4),
@@ -689,10 +801,127 @@ def run_ours(args, dist: Dist) -> int:
         "gpu_launches": head["gpu_launches"],
         "clocks": head["clocks"],
         "k_sweep": head["k_sweep"],
+        "f32": dict(_brief(head32), value=round(head32["us_per_iter"], 4), dtype="f32",
+                    k_sweep=head32["k_sweep"]) if head32 else None,
         "configs": extra,
     }
-    if dist.rank == 0:
-        print(json.dumps(line), flush=True)
+
+
+def scale_line(r64: dict, r32, single, args, world: int, shared: bool) -> dict:
+    """The N > 1 line: strong scaling of the sharded config, max over ranks."""
+    return {
+        "metric": METRIC,
+        "value": round(r64["us_per_iter"], 3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(r64["ms_per_step"], 3),
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": r64["dtype"],
+        "data": DATA,
+        "config": config_of(r64["name"], r64["dtype"], world),
+        "impl_detail": {
+            "step": "one full run: graph build T_C + N/K graph launches of every rank; value = max over ranks "
+                    "of the step time / N (the whole grid's iterations)",
+            "batch_size": r64["batch_size"],
+            "parallelism": f"axis-0 slabs x{world}, one process per GPU"
+                           + (" (ranks share GPUs on this box: protocol check only, not a scaling number)"
+                              if shared else ""),
+            "exchange": r64["exchange"],
+        },
+        "roofline": r64["roofline"],
+        "cpu_baseline": None,
+        "e2e": r64["e2e"],
+        "gpu_launches": r64["gpu_launches"] * world,
+        "clocks": r64["clocks"],
+        "single_gpu": single,
+        "f32": ({"value": round(r32["us_per_iter"], 3), "ms_per_step": round(r32["ms_per_step"], 3),
+                 "roofline": r32["roofline"], "e2e": r32["e2e"]} if r32 else None),
+    }
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--only", choices=sorted(CONFIGS), default=None,
+                    help="measure just this config (as the headline)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the non-headline configs")
+    ap.add_argument("--no-f32", action="store_true", help="skip the binary32 runs")
+    ap.add_argument("--quick", action="store_true", help="small K sweep")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU baseline work")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    dist = Dist(need_gpu=args.impl == "ours")
+    world = dist.world if "WORLD_SIZE" in os.environ else args.gpus
+    try:
+        if args.impl == "reference":
+            return run_reference(args, dist, world)
+        return run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+def run_ours(args, dist: Dist) -> int:
+    from paper_2501_09398_b200 import _lib
+
+    _lib.lib()
+    if _lib.device_count() < 1:
+        raise RuntimeError("bench.py needs a CUDA device (no CPU fallback)")
+    if dist.world > 1:
+        name = args.only or SCALED
+        r64 = measure_dist(name, CONFIGS[name], HEAD_DTYPE, args, dist)
+        log(f"[{name} x{dist.world} f64] {r64['us_per_iter']:.3f} us/iter")
+        r32 = None
+        if not args.no_f32:
+            r32 = measure_dist(name, CONFIGS[name], "f32", args, dist)
+            log(f"[{name} x{dist.world} f32] {r32['us_per_iter']:.3f} us/iter")
+        single = None
+        dist.barrier()
+        if dist.rank == 0 and os.environ.get("IB_BENCH_SINGLE", "1") != "0":
+            single = measure_single_gpu(name, CONFIGS[name], HEAD_DTYPE, args)
+            log(f"[{name} x1 f64] {single['value']:.3f} us/iter")
+        dist.barrier()
+        if dist.rank == 0:
+            print(json.dumps(scale_line(r64, r32, single, args, dist.world, dist.shared)), flush=True)
+        return 0
+    device = dist.local
+    name = args.only or HEADLINE
+    head = measure_ours(name, CONFIGS[name], HEAD_DTYPE, args, dist, device, headline=True)
+    log(f"[{name} f64] {head['us_per_iter']:.3f} us/iter at K={head['batch_size']} "
+        f"(stream {head['stream_us_per_iter']:.3f}, x{head['speedup_vs_stream']:.2f})")
+    head32 = None
+    if not args.no_f32:
+        head32 = measure_ours(name, CONFIGS[name], "f32", args, dist, device, headline=True)
+        log(f"[{name} f32] {head32['us_per_iter']:.3f} us/iter at K={head32['batch_size']} "
+            f"(stream {head32['stream_us_per_iter']:.3f}, x{head32['speedup_vs_stream']:.2f})")
+    extra = {}
+    if not args.no_extra and args.only is None:
+        for other, cfg in CONFIGS.items():
+            if other == name:
+                continue
+            extra[other] = {}
+            for dtype in (("f64",) if args.no_f32 else ("f32", "f64")):
+                try:
+                    r = measure_ours(other, cfg, dtype, args, dist, device, headline=False)
+                    r.pop("k_sweep", None)
+                    extra[other][dtype] = r
+                    log(f"[{other} {dtype}] {r['us_per_iter']:.3f} us/iter at K={r['batch_size']} "
+                        f"(stream {r['stream_us_per_iter']:.3f}, x{r['speedup_vs_stream']:.2f}) "
+                        f"roofline {r['roofline']['frac']:.3f}")
+                except MemoryError as exc:
+                    extra[other][dtype] = {"skipped": f"out of device memory: {exc}"}
+    cpu = cpu_baseline(name, args.cpu_budget) if dist.rank == 0 else None
+    print(json.dumps(head_line(head, head32, extra, cpu, args)), flush=True)
     return 0
 
 

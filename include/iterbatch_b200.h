@@ -59,7 +59,9 @@ extern "C" {
 #define IB_FLAG_DEVICE_LAUNCH 0x2 /* instantiate with cudaGraphInstantiateFlagDeviceLaunch (Listing 3) */
 #define IB_FLAG_NO_UPLOAD 0x4     /* skip cudaGraphUpload (first launch pays the upload) */
 #define IB_FLAG_WHILE 0x8         /* wrap the K-chain in a conditional WHILE node: one cudaGraphLaunch
-                                     runs all num_batches batches (device-side loop, no host gap) */
+                                     runs all num_batches batches (device-side loop, no host gap);
+                                     an odd K on a ping-pong solver puts two batches in the body, the
+                                     second (other buffer parity) inside an IF node */
 #define IB_FLAG_MEMINFO 0x10      /* fill ib_times.graph_bytes from cudaMemGetInfo before/after the
                                      build (the paper's m_base/m_node probe; costs ~ms per call) */
 #define IB_FLAG_PATCH 0x20        /* odd batch_size on a ping-pong solver: ONE executable whose kernel
@@ -213,7 +215,9 @@ int ib_slab_info(const ib_ctx *ctx, int64_t *lo, int64_t *hi, int *has_top, int 
  * output plane straight into the neighbours' halo planes (NVLink peer stores); ordering across
  * processes is a pair of one-thread kernels per iteration (wait for the neighbours' completed-
  * iteration counters, publish this rank's), all inside the iteration-batch graph. A lost
- * neighbour traps after IB_DIST_TIMEOUT_MS (default 20000) instead of hanging the device.
+ * neighbour traps after the wait timeout instead of hanging the device: ib_set_dist_timeout
+ * (milliseconds, > 0; initial value IB_DIST_TIMEOUT_MS, default 120000). It applies to graphs
+ * built afterwards (the timeout is a kernel argument baked into the graph's wait nodes).
  * A neighbour's first kernel of a run stores into this rank's halo planes, so the ranks must
  * synchronise (any host barrier) after ib_upload and before the next run; a run itself ends only
  * once the neighbours are done, so downloads need no barrier.
@@ -221,6 +225,7 @@ int ib_slab_info(const ib_ctx *ctx, int64_t *lo, int64_t *hi, int *has_top, int 
 #define IB_IPC_BYTES 192
 int ib_ipc_export(const ib_ctx *ctx, void *out, size_t bytes);
 int ib_ipc_attach(ib_ctx *ctx, const void *up_handles, const void *down_handles);
+int ib_set_dist_timeout(ib_ctx *ctx, int64_t milliseconds);
 
 /* ---- real traces (the reference's EventTrace schema, simulate.py:28-36, fileio.py:48) ---------
  * ib_trace_enable(ctx, capacity > 0) clears and arms tracing; 0 disarms. While armed (single-slab

@@ -87,6 +87,7 @@ PROTOTYPES = [
     ("ib_set_halo_mode", _I, [_P, _I]),
     ("ib_ipc_export", _I, [_P, _P, _SZ]),
     ("ib_ipc_attach", _I, [_P, _P, _P]),
+    ("ib_set_dist_timeout", _I, [_P, ctypes.c_int64]),
     ("ib_trace_enable", _I, [_P, _I64]),
     ("ib_trace_kernels", _I64, [_P, ctypes.POINTER(_I64), _I64]),
     ("ib_trace_host_events", _I64, [_P, ctypes.POINTER(_I64), _I64]),

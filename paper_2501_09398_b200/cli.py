@@ -173,9 +173,9 @@ def _cmd_sweep(args) -> int:
     # The driver grows its graph-executable memory the first time a process instantiates a graph
     # of a new size (tens of ms once; tools/build_phases.py) — a per-process cost, not part of
     # T_C(K) — so it is paid before the sweep, as bench.py does.
-    warm = wl._solver_for(state, args.dtype, args.devices, args.fuse)
-    warm.build_graph(max(sizes), build=args.build, pdl=args.pdl)
-    warm.destroy_graph()
+    with wl._solver(state, args.dtype, args.devices, args.fuse) as warm:
+        warm.build_graph(max(sizes), build=args.build, pdl=args.pdl)
+        warm.destroy_graph()
     creation, execution, stream, summary = [], [], [], []
     for k in sizes:
         plan = BatchPlan.from_batch_size(total, k)

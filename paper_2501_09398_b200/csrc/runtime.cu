@@ -254,6 +254,7 @@ static int create_common(ib_ctx **out, int solver, int dtype, const int64_t *dim
   for (int i = 0; i < nscalars; ++i) c->scalars[i] = scalars[i];
   c->rank = rank;
   c->nranks = nranks;
+  c->dist_timeout_ms = std::max<int64_t>(1, env_int("IB_DIST_TIMEOUT_MS", 120000));
   if ((solver == IB_SOLVER_FDTD || solver == IB_SOLVER_FDTD_FUSED) && !(scalars[0] > 0.0)) {
     delete c;
     return fail(IB_EINVAL, "cell_size must be positive");
@@ -378,6 +379,13 @@ int ib_ipc_attach(ib_ctx *c, const void *up, const void *dn) {
   c->peer_rows_up = (int)(rows * c->rank / c->nranks - rows * (c->rank - 1) / c->nranks);
   c->peer_rows_dn = (int)(rows * (c->rank + 2) / c->nranks - rows * (c->rank + 1) / c->nranks);
   c->peer = true;
+  return IB_OK;
+}
+
+int ib_set_dist_timeout(ib_ctx *c, int64_t ms) {
+  IB_TRY(check_ctx(c));
+  if (ms <= 0) return fail(IB_EINVAL, "the wait timeout must be > 0 ms");
+  c->dist_timeout_ms = ms;
   return IB_OK;
 }
 
@@ -798,14 +806,13 @@ int ib_graph_run(ib_ctx *c, int64_t num_batches, ib_times *tm) {
   IB_CUDA(cudaEventRecord(c->t0, c->stream()));
   if (num_batches > 0) {
     if (wh) {
-      if (c->ping_pong() && (c->K & 1) && num_batches > 1)
-        return fail(IB_EINVAL, "IB_FLAG_WHILE with an odd batch_size needs num_batches <= 1 (ping-pong parity)");
+      if (num_batches > INT32_MAX) return fail(IB_EINVAL, "IB_FLAG_WHILE: num_batches must fit the device counter");
       int nb = (int)num_batches;
       IB_CUDA(cudaMemcpyAsync(c->d_counter, &nb, sizeof(int), cudaMemcpyHostToDevice, c->stream()));
       c->ev(IB_EV_GRAPH_LAUNCHED, 0);
       IB_CUDA(cudaGraphLaunch(c->exec[c->cur], c->stream()));
       t.launches = 1;
-      if (c->ping_pong() && (c->K & 1)) c->cur ^= 1;
+      if (c->ping_pong() && (c->K & 1) && (num_batches & 1)) c->cur ^= 1;
     } else {
       for (int64_t b = 0; b < num_batches; ++b) {
         c->ev(IB_EV_GRAPH_LAUNCHED, b);

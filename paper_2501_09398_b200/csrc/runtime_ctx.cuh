@@ -31,6 +31,7 @@ struct ib_ctx {
   std::vector<cudaGraphNode_t> kernel_nodes;
   int exec_parity = 0;
   cudaGraphConditionalHandle cond[2] = {};
+  cudaGraphConditionalHandle cond_if[2] = {};  // odd-K WHILE: the IF node of the body's second batch
   int *d_counter = nullptr;  // WHILE-mode remaining-batch counter
   void *flush = nullptr;
   size_t flush_bytes = 0;
@@ -46,6 +47,7 @@ struct ib_ctx {
   int peer_rows_up = 0;  // the up neighbour's owned rows (locates its bottom halo plane)
   int peer_rows_dn = 0;  // the down neighbour's (FDTD: its lattice field stride)
   bool peer = false;
+  int64_t dist_timeout_ms = 120000;  // k_dist_wait traps after this long (ib_set_dist_timeout)
   // single-process slabs: halo planes by cudaMemcpyPeerAsync after each kernel (IB_HALO_COPY)
   // instead of the kernel's own stores into the neighbours' halos
   bool halo_copy = false;

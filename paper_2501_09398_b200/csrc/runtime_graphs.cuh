@@ -51,7 +51,7 @@ int nccl_exchange(ib_ctx *c, int parity, cudaStream_t st) {
 int launch_dist_wait(ib_ctx *c, cudaStream_t st) {
   const int top = c->slabs[0].has_top, bot = c->slabs[0].has_bot;
   Launch L = make_launch((const void *)ib::k_dist_wait, dim3(1), dim3(1), 0, (const unsigned long long *)c->sync,
-                         top, bot, (long long)env_int("IB_DIST_TIMEOUT_MS", 20000));
+                         top, bot, (long long)c->dist_timeout_ms);
   return launch_one(L, st, false);
 }
 int launch_dist_signal(ib_ctx *c, cudaStream_t st) {
@@ -265,6 +265,16 @@ __global__ void k_while_tick(int *counter, cudaGraphConditionalHandle h) {
   cudaGraphSetConditional(h, left > 0 ? 1u : 0u);
 }
 
+// Odd K on a ping-pong solver: the WHILE body holds two batches, the second (other start parity)
+// inside an IF node. This tick ends the first: it runs the IF body only if batches remain, and
+// stops the loop unless the IF body's own tick (k_while_tick) re-arms it.
+__global__ void k_while_tick_half(int *counter, cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hi) {
+  int left = *counter - 1;
+  *counter = left;
+  cudaGraphSetConditional(hi, left > 0 ? 1u : 0u);
+  cudaGraphSetConditional(hw, 0u);
+}
+
 namespace {
 
 // Build one executable graph starting at `parity`.
@@ -296,17 +306,46 @@ int build_one(ib_ctx *c, int parity, ib_times *tm) {
     cudaGraphNode_t last = nullptr;
     IB_TRY(build_manual_chain(c, body, c->K, parity, pdl, nullptr, &last, &nodes));
     if (wh) {
-      cudaKernelNodeParams np = {};
+      // An odd K flips a ping-pong solver's parity every batch, and one executable bakes in one
+      // start parity: the body then runs batch (parity) and, in an IF node, batch (parity ^ 1).
+      const bool two = c->ping_pong() && (c->K & 1);
       int *cnt = c->d_counter;
-      cudaGraphConditionalHandle h = c->cond[parity];
-      void *args[2] = {&cnt, &h};
-      np.func = (void *)k_while_tick;
+      cudaGraphConditionalHandle hw = c->cond[parity], hi = {};
+      cudaKernelNodeParams np = {};
       np.gridDim = dim3(1);
       np.blockDim = dim3(1);
-      np.kernelParams = args;
       cudaGraphNode_t tick;
-      IB_CUDA(cudaGraphAddKernelNode(&tick, body, &last, 1, &np));
-      ++nodes;
+      if (!two) {
+        void *args[2] = {&cnt, &hw};
+        np.func = (void *)k_while_tick;
+        np.kernelParams = args;
+        IB_CUDA(cudaGraphAddKernelNode(&tick, body, &last, 1, &np));
+        ++nodes;
+      } else {
+        IB_CUDA(cudaGraphConditionalHandleCreate(&c->cond_if[parity], g, 0, cudaGraphCondAssignDefault));
+        hi = c->cond_if[parity];
+        void *args[3] = {&cnt, &hw, &hi};
+        np.func = (void *)k_while_tick_half;
+        np.kernelParams = args;
+        IB_CUDA(cudaGraphAddKernelNode(&tick, body, &last, 1, &np));
+        cudaGraphNodeParams ip = {};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = hi;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t inode;
+        IB_CUDA(cudaGraphAddNode(&inode, body, &tick, 1, &ip));
+        cudaGraph_t second = ip.conditional.phGraph_out[0];
+        cudaGraphNode_t last2 = nullptr;
+        IB_TRY(build_manual_chain(c, second, c->K, parity ^ 1, pdl, nullptr, &last2, &nodes));
+        void *args2[2] = {&cnt, &hw};
+        cudaKernelNodeParams np2 = np;
+        np2.func = (void *)k_while_tick;
+        np2.kernelParams = args2;
+        cudaGraphNode_t tick2;
+        IB_CUDA(cudaGraphAddKernelNode(&tick2, second, &last2, 1, &np2));
+        nodes += 3;
+      }
     }
   } else {
     if (wh) return fail(IB_EINVAL, "IB_FLAG_WHILE requires IB_BUILD_MANUAL on a single slab");

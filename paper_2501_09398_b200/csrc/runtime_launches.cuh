@@ -20,6 +20,8 @@ int hotspot_rows_per_chunk(const ib_ctx *c, int rows) {
     rpc = (rows + chunks - 1) / chunks;
     rpc = std::min<int64_t>(rpc, 64);
   }
+  // grid.y = ceil(rows / rpc) must stay <= 65535 (tall, narrow grids: e.g. 100000 x 4)
+  rpc = std::max<int64_t>(rpc, (rows + 65534) / 65535);
   return (int)std::max<int64_t>(1, std::min<int64_t>(rpc, rows));
 }
 
@@ -42,7 +44,7 @@ int tma_groups(const ib_ctx *c) {  // G such that TM = G*V*256 holds whole y-row
 }
 
 template <typename T>
-HotKernel hotspot_variant(const ib_ctx *c, int rows) {
+HotKernel hotspot_variant(const ib_ctx *c, int g, int rows) {
   constexpr int V = 16 / sizeof(T);
   const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
   const int64_t M = c->plane();
@@ -56,7 +58,14 @@ HotKernel hotspot_variant(const ib_ctx *c, int rows) {
     if (!std::strcmp(force, "vec") && vec_ok) return HotKernel::Vec;
     if (!std::strcmp(force, "scalar")) return HotKernel::Scalar;
   }
-  const int64_t state_bytes = 3 * M * c->dims[0] * (int64_t)sizeof(T);
+  // the bytes that share this slab's L2: every slab on the same device, halo planes included
+  // (one rank of a multi-process run holds only its own slab)
+  int64_t planes = 0;
+  const bool multi = c->slabs.size() > 1 || c->dist();
+  for (const Slab &s : c->slabs)
+    if (s.device == c->slabs[g].device) planes += s.rows() + (multi ? 2 : 0);
+  if (planes == 0) planes = rows;
+  const int64_t state_bytes = 3 * M * planes * (int64_t)sizeof(T);
   // the state (T twice + P) against the 126 MB L2: measured crossover (tools/hotspot_vec_vs_tma.py,
   // us/iter vec / tma): 3-D 1024^2x8 (100.7 MB) 16.3 / 19.0, 1280x1024x8 (126 MB) 22.6 / 22.5,
   // 1536x1024x8 27.1 / 25.7; 2-D 2048^2 (50 MB) 8.3 / 8.9, 3072^2 (113 MB) 19.3 / 18.0.
@@ -124,7 +133,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
     const int top = (int)s.has_top, bot = (int)s.has_bot;
     const int fsys = (int)(c->dist() && c->peer);  // system-scope fence after halo stores (kernels.cuh)
     dim3 block(256);
-    switch (hotspot_variant<T>(c, rows)) {
+    switch (hotspot_variant<T>(c, g, rows)) {
       case HotKernel::Vec: {
         // rows per thread (R+2 row loads per R outputs): with the neighbour loads (no shuffles)
         // R = 1 — the most threads, the shortest per-thread chain — unless the grid would exceed

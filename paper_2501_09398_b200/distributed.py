@@ -99,7 +99,8 @@ class DistributedSolver(DeviceSolver):
     """
 
     def __init__(self, state, dtype, rank: int, world: int, device: int, uid: bytes | None = None,
-                 upload: bool = True, exchange: str = "nccl", allgather=None, fuse: bool = False):
+                 upload: bool = True, exchange: str = "nccl", allgather=None, fuse: bool = False,
+                 timeout_ms: int | None = None):
         kind = _kind_of_state(state)
         if kind not in ("hotspot2d", "hotspot3d", "fdtd"):
             raise ValueError("distributed execution is defined for hotspot grids and FDTD")
@@ -137,6 +138,8 @@ class DistributedSolver(DeviceSolver):
                                     _lib.DTYPE[self.dtype], dims,
                                     len(self.dims), sc, len(self.scalars), device, rank, world, idp))
         self._ctx = ctx
+        if timeout_ms is not None:  # the in-graph wait kernel's trap deadline (ib_set_dist_timeout)
+            _lib.check(L.ib_set_dist_timeout(ctx, int(timeout_ms)))
         self._allgather = allgather if (world > 1 and exchange == "peer") else None
         if self._allgather is not None:
             self._attach_peers(allgather)
@@ -225,11 +228,27 @@ class DistributedSolver(DeviceSolver):
     def build_graph(self, batch_size: int, build: str = "capture", pdl: bool = False,
                     device_launch: bool = False, upload: bool = True,
                     while_loop: bool = False, meminfo: bool = False) -> Times:
-        return super().build_graph(batch_size, "capture", pdl, False, upload, False, meminfo)
+        t = super().build_graph(batch_size, "capture", pdl, False, upload, False, meminfo)
+        if self._allgather is not None:
+            # peer exchange: a rank still capturing / instantiating would leave its neighbours'
+            # in-graph wait kernels spinning towards their trap deadline — no rank launches
+            # before every rank's graph exists (host barrier)
+            self._allgather(b"")
+        return t
 
     def run_batched(self, batch_size: int, num_batches: int, build: str = "capture",
                     pdl: bool = False, while_loop: bool = False) -> Times:
-        return super().run_batched(batch_size, num_batches, "capture", pdl, False)
+        """Build, (peer exchange: host barrier,) replay, destroy. ``gpu_s`` is T_C + T_E: the
+        device time of the launches plus the host time of the build (NCCL: one device interval
+        from before the build, as DeviceSolver.run_batched)."""
+        if self._allgather is None:
+            return super().run_batched(batch_size, num_batches, "capture", pdl, False)
+        tb = self.build_graph(batch_size, pdl=pdl)
+        te = self.run_graph(num_batches)
+        self.destroy_graph()
+        return Times(create_s=tb.create_s, instantiate_s=tb.instantiate_s, upload_s=tb.upload_s,
+                     build_s=tb.build_s + te.build_s, exec_s=te.exec_s, gpu_s=tb.build_s + te.gpu_s,
+                     kernels=te.kernels, launches=te.launches, nodes=tb.nodes)
 
     def local_temperature(self) -> np.ndarray:
         """This rank's owned rows [lo, hi) of the current temperature."""

@@ -33,8 +33,10 @@ from __future__ import annotations
 import ctypes
 import math
 import operator
+import threading
 import time
 from collections import OrderedDict
+from contextlib import contextmanager
 from dataclasses import dataclass
 from enum import Enum
 
@@ -551,30 +553,48 @@ def _rebuild(template, arrs):
 
 _CACHE: "OrderedDict[tuple, DeviceSolver]" = OrderedDict()
 _CACHE_SIZE = 2
+_CACHE_LOCK = threading.Lock()
 
 
-def _solver_for(state, dtype, devices, fuse: bool = False, halo: str = "store") -> DeviceSolver:
-    """A (cached) device context for this state's shape, with the state uploaded."""
+@contextmanager
+def _solver(state, dtype, devices, fuse: bool = False, halo: str = "store"):
+    """Check out a device context for this state's shape, with the state uploaded.
+
+    The reference functions are pure and thread-safe, so the cache of live contexts is too: a
+    context is removed from the cache while a call uses it (two threads on the same shape get two
+    contexts), and only contexts sitting in the cache are ever evicted and closed.
+    """
     kind = _kind_of_state(state)
     dt = _norm_dtype(dtype)
     dims, scalars = _dims_scalars(kind, state)
     devs = tuple(devices) if devices else ()
     key = (kind, dt, dims, scalars, devs, bool(fuse), halo)
-    s = _CACHE.pop(key, None)
+    with _CACHE_LOCK:
+        s = _CACHE.pop(key, None)
     if s is None:
-        while len(_CACHE) >= _CACHE_SIZE:
-            _, old = _CACHE.popitem(last=False)
-            old.close()
         s = DeviceSolver(state, dt, devs, upload=False, fuse=fuse, halo=halo)
-    _CACHE[key] = s
-    s.upload(state)
-    return s
+    try:
+        s.upload(state)
+        yield s
+    finally:
+        evicted = []
+        with _CACHE_LOCK:
+            if key in _CACHE:  # another thread checked in the same shape meanwhile: keep one
+                evicted.append(s)
+            else:
+                _CACHE[key] = s
+                while len(_CACHE) > _CACHE_SIZE:
+                    evicted.append(_CACHE.popitem(last=False)[1])
+        for old in evicted:
+            old.close()
 
 
 def release_cached_contexts() -> None:
-    """Free the device memory held by cached solver contexts."""
-    while _CACHE:
-        _, s = _CACHE.popitem()
+    """Free the device memory held by cached (checked-in) solver contexts."""
+    with _CACHE_LOCK:
+        items = list(_CACHE.values())
+        _CACHE.clear()
+    for s in items:
         s.close()
 
 
@@ -582,9 +602,9 @@ def release_cached_contexts() -> None:
 # Step protocol (per-step API parity; each call is upload -> 1 kernel -> download)
 # ================================================================================================
 def _one_step(w, step: int, writes, dtype="f64"):
-    s = _solver_for(w, dtype, None)
-    s.run_step(step)
-    return s.download(w, fields=writes)
+    with _solver(w, dtype, None) as s:
+        s.run_step(step)
+        return s.download(w, fields=writes)
 
 
 def vector_scale_step(w, workers: int | None = None, *, dtype="f64"):
@@ -677,9 +697,9 @@ def run_loop(program, state, total_iterations: int, workers=None, *, dtype="f64"
     _check_program(program, state)
     if total == 0:
         return state
-    s = _solver_for(state, dtype, devices, fuse, halo)
-    s.run_stream(total, pdl=pdl)
-    return s.download(state, fields=_written_fields(state))
+    with _solver(state, dtype, devices, fuse, halo) as s:
+        s.run_stream(total, pdl=pdl)
+        return s.download(state, fields=_written_fields(state))
 
 
 def run_batched(program, state, batch_size: int, num_batches: int, workers=None, *, dtype="f64",
@@ -699,11 +719,11 @@ def run_batched(program, state, batch_size: int, num_batches: int, workers=None,
     _check_program(program, state)
     if num == 0:
         return state
-    s = _solver_for(state, dtype, devices, fuse, halo)
-    s.build_graph(size, build=build, pdl=pdl, while_loop=while_loop, patch=patch)
-    s.run_graph(num)
-    s.destroy_graph()
-    return s.download(state, fields=_written_fields(state))
+    with _solver(state, dtype, devices, fuse, halo) as s:
+        s.build_graph(size, build=build, pdl=pdl, while_loop=while_loop, patch=patch)
+        s.run_graph(num)
+        s.destroy_graph()
+        return s.download(state, fields=_written_fields(state))
 
 
 def run_peeled(program, state, total_iterations: int, batch_size: int, workers=None, *,
@@ -723,9 +743,9 @@ def run_peeled(program, state, total_iterations: int, batch_size: int, workers=N
     _check_program(program, state)
     if total == 0:
         return state
-    s = _solver_for(state, dtype, devices, fuse, halo)
-    s.run_peeled(total, size, build=build, pdl=pdl)
-    return s.download(state, fields=_written_fields(state))
+    with _solver(state, dtype, devices, fuse, halo) as s:
+        s.run_peeled(total, size, build=build, pdl=pdl)
+        return s.download(state, fields=_written_fields(state))
 
 
 def _written_fields(state):
@@ -774,32 +794,32 @@ def time_workload_phases(program, state, plan, order, repeats: int = 10, *, dtyp
     if reps < 1:
         raise ValueError("repeats must be >= 1")
     _check_program(program, state)
-    s = _solver_for(state, dtype, devices, fuse)
-    out = {"creation": [], "execution": [], "total": [], "gpu": [], "times": []}
-    batched = _order_value(order) == ExecutionOrder.BATCHED.value
-    for r in range(reps):
-        if r:
-            s.upload(state)
-        if batched:
-            t0 = time.perf_counter()
-            tb = s.build_graph(plan.batch_size, build=build, pdl=pdl, while_loop=while_loop,
-                               meminfo=meminfo and r == 0, patch=patch)
-            te = s.run_graph(plan.num_batches)
-            total = time.perf_counter() - t0
-            s.destroy_graph()
-            out["creation"].append(tb.build_s)
-            out["execution"].append(te.exec_s)
-            out["times"].append((tb, te))
-        else:
-            t0 = time.perf_counter()
-            te = s.run_stream(plan.total_kernel_executions, pdl=pdl)
-            total = time.perf_counter() - t0
-            out["creation"].append(0.0)
-            out["execution"].append(te.exec_s)
-            out["times"].append((None, te))
-        out["total"].append(total)
-        out["gpu"].append(te.gpu_s)
-    return out
+    with _solver(state, dtype, devices, fuse) as s:
+        out = {"creation": [], "execution": [], "total": [], "gpu": [], "times": []}
+        batched = _order_value(order) == ExecutionOrder.BATCHED.value
+        for r in range(reps):
+            if r:
+                s.upload(state)
+            if batched:
+                t0 = time.perf_counter()
+                tb = s.build_graph(plan.batch_size, build=build, pdl=pdl, while_loop=while_loop,
+                                   meminfo=meminfo and r == 0, patch=patch)
+                te = s.run_graph(plan.num_batches)
+                total = time.perf_counter() - t0
+                s.destroy_graph()
+                out["creation"].append(tb.build_s)
+                out["execution"].append(te.exec_s)
+                out["times"].append((tb, te))
+            else:
+                t0 = time.perf_counter()
+                te = s.run_stream(plan.total_kernel_executions, pdl=pdl)
+                total = time.perf_counter() - t0
+                out["creation"].append(0.0)
+                out["execution"].append(te.exec_s)
+                out["times"].append((None, te))
+            out["total"].append(total)
+            out["gpu"].append(te.gpu_s)
+        return out
 
 
 # ================================================================================================

@@ -39,3 +39,12 @@ def gpu():
     if n < 1:
         pytest.fail("no CUDA device visible for a -m gpu test (no CPU fallback exists)")
     return n
+
+
+def spread(n: int) -> list:
+    """Device list for n axis-0 slabs: distinct GPUs when the box has them (peer access, cross-
+    device graph edges, NVLink halo stores), else all on GPU 0 — the same code path either way."""
+    from paper_2501_09398_b200 import _lib
+
+    count = max(1, _lib.device_count())
+    return [g % count for g in range(n)]

@@ -16,6 +16,7 @@ import pytest
 
 from oracle import cpu as ocpu
 from paper_2501_09398_b200 import workloads as wl
+from tests.conftest import spread
 
 pytestmark = pytest.mark.gpu
 
@@ -74,7 +75,7 @@ def test_hotspot3d_2048_light_cone_windows_and_modes(gpu, big):
                    (127, 1024), (2000, 500)):
         _window_check(t, p, got, r0, c0, w, n)
     assert np.array_equal(got, _run(t, p, "stream", n))
-    assert np.array_equal(got, _run(t, p, 5, n, devices=[0, 0, 0]))
+    assert np.array_equal(got, _run(t, p, 5, n, devices=spread(3)))
 
 
 @pytest.fixture(scope="module")

@@ -6,6 +6,7 @@ import pytest
 
 from oracle import cpu as ocpu
 from paper_2501_09398_b200 import workloads as wl
+from tests.conftest import spread
 
 pytestmark = pytest.mark.gpu
 
@@ -33,7 +34,7 @@ def test_fuzz_hotspot(gpu, dtype):
         pdl = bool(rng.integers(2))
         want = ocpu.hotspot(st.temperature, st.power, k, kk * nb, npd)
         got = wl.run_batched(wl.hotspot_program(), st, kk, nb, dtype=dtype, pdl=pdl and slabs == 1,
-                             devices=[0] * slabs if slabs > 1 else None,
+                             devices=spread(slabs) if slabs > 1 else None,
                              build="capture" if slabs > 1 else "manual").temperature
         assert np.array_equal(np.asarray(got, npd), want), (c, shape, k, kk, nb, slabs, pdl)
     wl.release_cached_contexts()
@@ -56,7 +57,7 @@ def test_fuzz_fdtd(gpu, dtype):
         want = ocpu.fdtd(st.state_arrays(), d, dt / wl.VACUUM_PERMEABILITY, dt / wl.VACUUM_PERMITTIVITY,
                          kk * nb, npd)
         got = wl.run_batched(wl.fdtd_program(), st, kk, nb, dtype=dtype, fuse=fuse,
-                             devices=[0] * slabs if slabs > 1 else None,
+                             devices=spread(slabs) if slabs > 1 else None,
                              build="capture" if slabs > 1 else "manual").state_arrays()
         for g, w in zip(got, want):
             assert np.array_equal(np.asarray(g, npd), w), (c, dims, d, kk, nb, fuse, slabs)

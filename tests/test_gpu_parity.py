@@ -16,6 +16,7 @@ import pytest
 
 from paper_2501_09398_b200 import cli
 from paper_2501_09398_b200 import workloads as wl
+from tests.conftest import spread
 from paper_2501_09398_b200.model import feasible_batch_sizes
 from oracle import cpu as ocpu
 
@@ -65,8 +66,6 @@ def test_p0_graph_variants_match_reference(gpu, kat, variant):
     n, k = kat["iterations"], kat["batch_size"]
     kw = {"build": "capture" if variant.startswith("capture") else "manual",
           "pdl": "pdl" in variant, "while_loop": variant == "while"}
-    if variant == "while" and k % 2 == 1 and kat["workload"].startswith("hotspot") and n // k > 1:
-        pytest.skip("WHILE with odd K on a ping-pong grid runs one batch per launch")
     out = wl.run_batched(_program(kat["workload"]), state, k, n // k, **kw)
     assert f"{wl.state_checksum(out):016x}" == kat["checksum"]
 
@@ -188,7 +187,7 @@ def test_p3_slabs_bit_identical_to_single_device(gpu, shape, slabs, dtype):
     state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
     prog = wl.hotspot_program()
     ref = wl.state_checksum(wl.run_loop(prog, state, 10, dtype=dtype))
-    devs = [0] * slabs
+    devs = spread(slabs)  # distinct GPUs when the box has them (peer stores)
     assert wl.state_checksum(wl.run_loop(prog, state, 10, dtype=dtype, devices=devs)) == ref
     for k, build in ((5, "capture"), (2, "capture"), (10, "manual")):
         got = wl.run_batched(prog, state, k, 10 // k, dtype=dtype, devices=devs, build=build)

@@ -16,6 +16,7 @@ import pytest
 
 from oracle import cpu as ocpu
 from paper_2501_09398_b200 import workloads as wl
+from tests.conftest import spread
 
 pytestmark = pytest.mark.gpu
 
@@ -94,7 +95,7 @@ def test_hotspot_variants_with_slabs(gpu, env, kernel, slabs):
     for shape in ((30, 12, 8), (41, 64)):
         state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
         want = ocpu.hotspot(state.temperature, state.power, 0.1, 6, np.float64)
-        got = wl.run_batched(wl.hotspot_program(), state, 3, 2, devices=[0] * slabs, build="capture")
+        got = wl.run_batched(wl.hotspot_program(), state, 3, 2, devices=spread(slabs), build="capture")
         assert np.array_equal(got.temperature, want), shape
 
 
@@ -109,7 +110,7 @@ def test_hotspot_slabs_copy_exchange(gpu, env, kernel, slabs):
     for shape in ((30, 12, 8), (41, 64)):
         state = wl.HotspotWorkload(rng.random(shape), rng.random(shape) * 1e-3, 0.1)
         want = ocpu.hotspot(state.temperature, state.power, 0.1, 6, np.float64)
-        with wl.DeviceSolver(state, "f64", devices=[0] * slabs, halo="copy") as s:
+        with wl.DeviceSolver(state, "f64", devices=spread(slabs), halo="copy") as s:
             d = s.describe()  # kernels plus the peer-copy nodes after each (2 per interior slab)
             assert sum(e.get("memcpy_nodes", 0) for e in d) == 2 * (slabs - 1)
             s.run_stream(6)
@@ -122,11 +123,11 @@ def test_hotspot_slabs_copy_exchange(gpu, env, kernel, slabs):
                 s.upload(state)
                 s.run_batched(k, n, build="capture", pdl=True)
                 assert np.array_equal(s.download(state).temperature, want), (shape, k)
-        got = wl.run_batched(wl.hotspot_program(), state, 3, 2, devices=[0] * slabs, build="capture",
+        got = wl.run_batched(wl.hotspot_program(), state, 3, 2, devices=spread(slabs), build="capture",
                              halo="copy")  # the module-level drivers take the option too
         assert np.array_equal(got.temperature, want), shape
-        with wl.DeviceSolver(state, "f32", devices=[0] * slabs, halo="copy") as s, \
-                wl.DeviceSolver(state, "f32", devices=[0] * slabs) as v2:
+        with wl.DeviceSolver(state, "f32", devices=spread(slabs), halo="copy") as s, \
+                wl.DeviceSolver(state, "f32", devices=spread(slabs)) as v2:
             s.run_batched(3, 2, build="capture")
             v2.run_batched(3, 2, build="capture")
             assert np.array_equal(s.download(state).temperature, v2.download(state).temperature)
@@ -139,7 +140,7 @@ def test_halo_mode_validation(gpu):
         wl.DeviceSolver(hot, "f32", halo="nvlink")
     with wl.DeviceSolver(hot, "f32", halo="copy") as s:  # one slab: accepted, nothing to exchange
         s.run_stream(2)
-    with wl.DeviceSolver(wl.fdtd_cavity(6, 4, 6), "f32", devices=[0, 0], halo="copy") as s:
+    with wl.DeviceSolver(wl.fdtd_cavity(6, 4, 6), "f32", devices=spread(2), halo="copy") as s:
         s.run_stream(2)  # FDTD slabs take the copy exchange too
 
 
@@ -155,11 +156,11 @@ def test_fdtd_slabs_peeled_and_per_step(gpu, fuse, halo):
     dt = state.time_step
     want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
                      dt / wl.VACUUM_PERMITTIVITY, 7, np.float64)
-    got = wl.run_peeled(wl.fdtd_program(), state, 7, 3, devices=[0, 0, 0], fuse=fuse, halo=halo,
+    got = wl.run_peeled(wl.fdtd_program(), state, 7, 3, devices=spread(3), fuse=fuse, halo=halo,
                         build="capture")
     for g, w in zip(got.state_arrays(), want):
         assert np.array_equal(g, w)
-    with wl.DeviceSolver(state, "f64", devices=[0, 0, 0], fuse=fuse, halo=halo) as s:
+    with wl.DeviceSolver(state, "f64", devices=spread(3), fuse=fuse, halo=halo) as s:
         for _ in range(7):
             for step in range(1 if fuse else 2):
                 s.run_step(step)
@@ -287,7 +288,7 @@ def test_fused_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
     dt = state.time_step
     want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
                      dt / wl.VACUUM_PERMITTIVITY, 6, npd)
-    devs = [0] * slabs
+    devs = spread(slabs)
     for tj, chunks in ((0, 0), (1, 2), (3, 1)):
         env(IB_FDTD_TJ=tj, IB_FDTD_CHUNKS=chunks)
         for k, n in ((3, 2), (2, 3)):
@@ -325,7 +326,7 @@ def test_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
     dt = state.time_step
     want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY,
                      dt / wl.VACUUM_PERMITTIVITY, 6, npd)
-    devs = [0] * slabs
+    devs = spread(slabs)
     for tj, chunks in ((0, 0), (1, 2), (3, 1)):
         env(IB_FDTD_TJ=tj, IB_FDTD_CHUNKS=chunks)
         got = wl.run_batched(wl.fdtd_program(), state, 3, 2, dtype=dtype, devices=devs, build="capture")
