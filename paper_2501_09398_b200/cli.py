@@ -176,7 +176,7 @@ def _cmd_sweep(args) -> int:
     with wl._solver(state, args.dtype, args.devices, args.fuse) as warm:
         warm.build_graph(max(sizes), build=args.build, pdl=args.pdl)
         warm.destroy_graph()
-    creation, execution, stream, summary = [], [], [], []
+    creation, execution, total_, stream, summary = [], [], [], [], []
     for k in sizes:
         plan = BatchPlan.from_batch_size(total, k)
         # an odd K on a ping-pong solver would otherwise build two executables (one per start
@@ -190,6 +190,7 @@ def _cmd_sweep(args) -> int:
                                     args.repeats, **kw)
         creation.append(MeasurementPoint(k, tuple(g["creation"])))
         execution.append(MeasurementPoint(k, tuple(g["execution"])))
+        total_.append(MeasurementPoint(k, tuple(c + e for c, e in zip(g["creation"], g["execution"]))))
         stream.append(MeasurementPoint(k, tuple(s["execution"])))
         row = {
             "batch_size": k,
@@ -211,11 +212,32 @@ def _cmd_sweep(args) -> int:
     write_measurements_csv(MeasurementSeries(tuple(creation), label), os.path.join(args.out, "creation.csv"))
     write_measurements_csv(MeasurementSeries(tuple(execution), label), os.path.join(args.out, "execution.csv"))
     write_measurements_csv(MeasurementSeries(tuple(stream), label), os.path.join(args.out, "stream.csv"))
+    # T = T_C + T_E per repeat: `iterbatch speedup --baseline stream.csv --graph total.csv`
+    write_measurements_csv(MeasurementSeries(tuple(total_), label), os.path.join(args.out, "total.csv"))
     with open(os.path.join(args.out, "summary.json"), "w") as fh:
         json.dump({"workload": args.workload, "size": args.size, "iterations": total,
                    "dtype": args.dtype, "build": args.build, "pdl": args.pdl, "fuse": args.fuse,
                    "rows": summary}, fh, indent=1)
     return 0
+
+
+def free_device_bytes(device: int) -> int:
+    import ctypes
+
+    from . import _lib
+
+    free = ctypes.c_int64()
+    _lib.check(_lib.lib().ib_mem_info(device, ctypes.byref(free), None))
+    return free.value
+
+
+def graph_bytes(solver, size: int, base_free: int) -> int:
+    """Device bytes held with a size-S graph instantiated: the free memory before the solver's
+    first build minus the free memory now (cudaMemGetInfo)."""
+    solver.build_graph(size)
+    used = base_free - free_device_bytes(solver.devices[0] if solver.devices else 0)
+    solver.destroy_graph()
+    return used
 
 
 def _cmd_trace(args) -> int:
@@ -225,22 +247,46 @@ def _cmd_trace(args) -> int:
     state = build_workload(args.workload, args.size)
     plan = BatchPlan.from_batch_size(args.iterations, args.batch_size)
     os.makedirs(args.out, exist_ok=True)
+    even = lambda x: max(2, x + (x & 1))  # noqa: E731
+    k = plan.batch_size
     with wl.DeviceSolver(state, args.dtype, devices=args.devices, fuse=args.fuse) as s:
+        # memory model m = m_base + m_node * S (model.py:130-142, memory_usage:266-269), probed
+        # before this context built any graph: free device memory before the first build minus
+        # free memory with the size-S graph instantiated — right whether the driver releases a
+        # destroyed graph's memory or keeps it for the next (bigger) one
+        msizes = sorted({even(k), even(2 * k), even(4 * k), even(8 * k)})
+        base = free_device_bytes(s.devices[0] if s.devices else 0)
+        mem = [graph_bytes(s, size, base) for size in msizes]
         s.run_batched(plan.batch_size, plan.num_batches, pdl=args.pdl)  # warm-up
         s.upload(state)
         g = tr.capture_graph(s, plan.batch_size, plan.num_batches, pdl=args.pdl)
         s.upload(state)
         st = tr.capture_stream(s, plan.total_kernel_executions)
-        # memory model m = m_base + m_node * nodes (model.py:130-142): two graph sizes
-        kpi = s.kernels_per_iteration
-        b1 = s.build_graph(plan.batch_size, meminfo=True).graph_bytes
-        s.destroy_graph()
-        b2 = s.build_graph(2 * plan.batch_size, meminfo=True).graph_bytes
-        s.destroy_graph()
+        # t_l: launch call -> first kernel start on an idle device (the traced run above queues
+        # launches behind each other, and its first traced launch pays CUPTI's set-up)
+        s.upload(state)
+        lat = tr.capture_launch_latency(s, plan.batch_size)
+        # k_c, b_c: the whole build time T_C (create + instantiate + upload, the phases the sweep
+        # and fit_creation use) at four batch sizes, least squares over the batch size S; even
+        # sizes so a ping-pong solver builds one executable per size
+        sizes = sorted({even(k // 2), even(k), even(2 * k), even(4 * k)})
+        tc = []
+        for size in sizes:
+            samples = []
+            for _ in range(3):
+                samples.append(s.build_graph(size).build_s)
+                s.destroy_graph()
+            tc.append(statistics.median(samples))
     params = tr.derive_parameters(g, st)
-    n1 = plan.batch_size * kpi
-    m_node = max(0, (b2 - b1) // n1)
-    memory = {"m_base": max(0, b1 - m_node * n1), "m_node": m_node}
+    params["t_l_traced_run"] = params["t_l"]
+    params["t_l"] = statistics.median(lat)
+    params["k_c_node_add"] = params["k_c"]
+    params["k_c"], params["b_c"] = tr.fit_line(sizes, tc)
+    params["b_c"] = max(0.0, params["b_c"])
+    params["creation_points"] = [[sz, t] for sz, t in zip(sizes, tc)]
+    m_node, m_base = tr.fit_line(msizes, mem)
+    memory = {"m_base": int(max(0.0, round(m_base))), "m_node": int(max(0.0, round(m_node)))}
+    params["memory_points"] = [[sz, b] for sz, b in zip(msizes, mem)]
     tr.write_trace_csv(g, os.path.join(args.out, "graph_trace.csv"))
     tr.write_trace_csv(st, os.path.join(args.out, "stream_trace.csv"))
     tr.write_params(os.path.join(args.out, "params.txt"), params, memory)

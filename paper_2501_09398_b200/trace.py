@@ -109,6 +109,34 @@ def capture_stream(solver, iterations: int, pdl: bool = False) -> RealTrace:
     return _assemble("baseline", 1, cap, kern, host)
 
 
+def capture_launch_latency(solver, batch_size: int, reps: int = 7) -> list:
+    """t_l, the first-launch latency of the model (model.py:48-74), measured as the paper defines
+    it: graph launch call -> first kernel start with the device idle. The graph is built first and
+    launched ``reps`` times, each launch synchronised before the next (ib_graph_run waits for its
+    end event), so no launch queues behind another; the CUPTI set-up of the first traced launch is
+    absorbed by _arm_warm. Returns the per-launch latencies in seconds."""
+    per = batch_size * solver.kernels_per_iteration
+    cap = reps * per
+    _arm_warm(solver, cap)
+    solver.build_graph(batch_size)
+    for _ in range(reps):
+        solver.run_graph(1)
+    solver.destroy_graph()
+    kern, host, n = _collect(solver, cap)
+    if n != cap:
+        raise RuntimeError(f"trace recorded {n} kernels, expected {cap}")
+    launches = sorted(int(t) for t, kind, _, _ in host if kind == 3)
+    return [(int(kern[i * per, 0]) - t) * 1e-9 for i, t in enumerate(launches)]
+
+
+def fit_line(xs, ys) -> tuple[float, float]:
+    """Least-squares slope and intercept."""
+    x = np.asarray(xs, dtype=np.float64)
+    y = np.asarray(ys, dtype=np.float64)
+    slope, intercept = np.polyfit(x, y, 1)
+    return float(slope), float(intercept)
+
+
 def _assemble(mode, size, num, kern, host) -> RealTrace:
     starts = [r for r in host if r[1] == BUILD_STARTED]
     t0 = int(starts[0][0]) if starts else int(min(host[0][0] if len(host) else kern[0, 0], kern[0, 0]))
@@ -151,8 +179,11 @@ def derive_parameters(graph: RealTrace, stream: RealTrace) -> dict:
     """The model's platform constants (model.py:48-74) measured from real traces.
 
     t_k kernel duration; t_i gap between consecutive kernels inside a graph; t_a gap between the
-    last kernel of a graph and the first of the next; t_l first launch call -> first kernel start;
-    t_b kernel-to-kernel gap of the plain launch loop; k_c / b_c per-node and fixed build cost.
+    last kernel of a graph and the first of the next; t_l first launch call -> first kernel start
+    of this run (the trace command replaces it with the idle-device measurement of
+    capture_launch_latency); t_b kernel-to-kernel gap of the plain launch loop; k_c / b_c here are
+    the node-add interval and the add->upload tail of ONE build (the trace command replaces them
+    with a fit of the whole build time T_C over several batch sizes, the phases the sweep fits).
     """
     g = graph.kernels
     size = graph.batch_size
