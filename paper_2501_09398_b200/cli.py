@@ -253,8 +253,10 @@ def _cmd_trace(args) -> int:
         # memory model m = m_base + m_node * S (model.py:130-142, memory_usage:266-269), probed
         # before this context built any graph: free device memory before the first build minus
         # free memory with the size-S graph instantiated — right whether the driver releases a
-        # destroyed graph's memory or keeps it for the next (bigger) one
-        msizes = sorted({even(k), even(2 * k), even(4 * k), even(8 * k)})
+        # destroyed graph's memory or keeps it for the next (bigger) one. cudaMemGetInfo moves in
+        # 2 MiB steps and a kernel node holds ~1-3 KB, so the probe sizes are thousands of nodes
+        # (not the run's K) for the fit to resolve m_node
+        msizes = [1000, 2000, 4000, 8000]
         base = free_device_bytes(s.devices[0] if s.devices else 0)
         mem = [graph_bytes(s, size, base) for size in msizes]
         s.run_batched(plan.batch_size, plan.num_batches, pdl=args.pdl)  # warm-up
@@ -277,9 +279,14 @@ def _cmd_trace(args) -> int:
                 samples.append(s.build_graph(size).build_s)
                 s.destroy_graph()
             tc.append(statistics.median(samples))
-    params = tr.derive_parameters(g, st)
+        params = tr.derive_parameters(g, st, s.kernels_per_iteration)
+        # t_l with no profiler attached (CUDA events), the value the params file carries; the
+        # CUPTI-measured idle-launch latency is reported beside it
+        s.upload(state)
+        t_l = tr.launch_latency_untraced(s, plan.batch_size, params["t_a"], params["t_k"])
     params["t_l_traced_run"] = params["t_l"]
-    params["t_l"] = statistics.median(lat)
+    params["t_l_cupti"] = statistics.median(lat)
+    params["t_l"] = t_l
     params["k_c_node_add"] = params["k_c"]
     params["k_c"], params["b_c"] = tr.fit_line(sizes, tc)
     params["b_c"] = max(0.0, params["b_c"])

@@ -20,6 +20,7 @@ This module records the real thing:
 from __future__ import annotations
 
 import ctypes
+import math
 import statistics
 from dataclasses import dataclass
 
@@ -83,18 +84,36 @@ def _collect(solver, capacity: int):
     return kern, rows[: 4 * m].reshape(-1, 4), int(n)
 
 
-def capture_graph(solver, batch_size: int, num_batches: int, pdl: bool = False) -> RealTrace:
-    """Build a batch_size-iteration graph and replay it num_batches times, traced."""
+def capture_graph(solver, batch_size: int, num_batches: int, pdl: bool = False, warm: int = 2) -> RealTrace:
+    """Build a batch_size-iteration graph and replay it num_batches times, traced.
+
+    The first launch of a newly instantiated executable under CUPTI kernel tracing pays CUPTI's
+    instrumentation of its nodes (~3 ms at 100 nodes, seen as a 3 ms first-launch latency), which an
+    untraced run never pays. So the executable is launched ``warm`` times first (two: both parity
+    executables of an odd K, and the state parity is unchanged) and those launches' kernel records
+    and launch events are dropped; the build events are kept."""
     kpi = solver.kernels_per_iteration
-    cap = batch_size * num_batches * kpi
+    per = batch_size * kpi
+    cap = per * (num_batches + warm)
     _arm_warm(solver, cap)
     solver.build_graph(batch_size, pdl=pdl)
+    solver.run_graph(warm)
     solver.run_graph(num_batches)
     solver.destroy_graph()
     kern, host, n = _collect(solver, cap)
     if n != cap:
         raise RuntimeError(f"trace recorded {n} kernels, expected {cap}")
-    return _assemble("graph", batch_size * kpi, num_batches, kern, host)
+    kern = kern[warm * per:]
+    keep, seen = [], 0
+    for row in host:
+        if row[1] == 3:  # graph_launched: drop the warm launches, renumber the rest from 0
+            seen += 1
+            if seen <= warm:
+                continue
+            row = row.copy()
+            row[2] = seen - warm - 1
+        keep.append(row)
+    return _assemble("graph", per, num_batches, kern, np.asarray(keep, dtype=np.int64))
 
 
 def capture_stream(solver, iterations: int, pdl: bool = False) -> RealTrace:
@@ -127,6 +146,24 @@ def capture_launch_latency(solver, batch_size: int, reps: int = 7) -> list:
         raise RuntimeError(f"trace recorded {n} kernels, expected {cap}")
     launches = sorted(int(t) for t, kind, _, _ in host if kind == 3)
     return [(int(kern[i * per, 0]) - t) * 1e-9 for i, t in enumerate(launches)]
+
+
+def launch_latency_untraced(solver, batch_size: int, t_a: float, t_k: float = 0.0, reps: int = 7) -> float:
+    """t_l without any profiler attached: the device time of ONE graph launch on an idle device
+    (CUDA events on the launch stream: the start event is stamped as soon as the host enqueues it,
+    before the launch call returns) minus the steady per-graph time of back-to-back launches, plus
+    the inter-graph gap t_a those back-to-back launches contain instead of t_l. The graph is cut
+    to ~200 us of kernels (at least 2 iterations, even) so the run-to-run noise of the execution
+    stays well below the latency being measured. Returns seconds."""
+    if t_k > 0:
+        short = max(2, int(math.ceil(200e-6 / t_k)))
+        batch_size = min(batch_size, short + (short & 1))
+    solver.build_graph(batch_size)
+    solver.run_graph(2)  # first launches of the executable(s)
+    steady = statistics.median(solver.run_graph(20).gpu_s / 20 for _ in range(3))
+    single = statistics.median(solver.run_graph(1).gpu_s for _ in range(reps))
+    solver.destroy_graph()
+    return max(0.0, single - steady + t_a)
 
 
 def fit_line(xs, ys) -> tuple[float, float]:
@@ -175,7 +212,15 @@ def write_trace_csv(trace: RealTrace, path) -> None:
             fh.write(f"{max(t, 0.0):.9f},{kind},{b},{k}\n")
 
 
-def derive_parameters(graph: RealTrace, stream: RealTrace) -> dict:
+def _per_iteration(k: np.ndarray, kpi: int) -> np.ndarray:
+    """[start, end] of each iteration (its first kernel's start, its last kernel's end)."""
+    if kpi <= 1:
+        return k
+    n = len(k) // kpi
+    return np.stack([k[0:n * kpi:kpi, 0], k[kpi - 1:n * kpi:kpi, 1]], axis=1)
+
+
+def derive_parameters(graph: RealTrace, stream: RealTrace, kernels_per_iteration: int = 1) -> dict:
     """The model's platform constants (model.py:48-74) measured from real traces.
 
     t_k kernel duration; t_i gap between consecutive kernels inside a graph; t_a gap between the
@@ -184,15 +229,21 @@ def derive_parameters(graph: RealTrace, stream: RealTrace) -> dict:
     capture_launch_latency); t_b kernel-to-kernel gap of the plain launch loop; k_c / b_c here are
     the node-add interval and the add->upload tail of ONE build (the trace command replaces them
     with a fit of the whole build time T_C over several batch sizes, the phases the sweep fits).
+
+    ``kernels_per_iteration`` > 1 (FDTD's H then E launches): the model's unit of work is one
+    iteration, as in the sweeps and fits (batch sizes count iterations), so t_k is an iteration's
+    span (first kernel start -> last kernel end, the H->E gap inside) and the gaps are between
+    iterations.
     """
-    g = graph.kernels
-    size = graph.batch_size
+    kpi = max(1, int(kernels_per_iteration))
+    g = _per_iteration(graph.kernels, kpi)
+    size = max(1, graph.batch_size // kpi)
     dur = g[:, 1] - g[:, 0]
     gaps = g[1:, 0] - g[:-1, 1]
     idx = np.arange(1, len(g))
     intra = gaps[(idx % size) != 0]
     inter = gaps[(idx % size) == 0]
-    s = stream.kernels
+    s = _per_iteration(stream.kernels, kpi)
     sgaps = s[1:, 0] - s[:-1, 1]
     launches = [e[0] for e in graph.events if e[1] == "graph_launched"]
     nodes = sorted(e[0] for e in graph.events if e[1] == "node_added")

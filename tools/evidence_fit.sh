@@ -6,6 +6,7 @@ mkdir -p gpurun_out/evidence
 # K sweeps (paper Sec. III-C: creation / execution / stream per feasible K, 5 repeats)
 sweep() { timeout 900 python -m paper_2501_09398_b200 sweep --workload $1 --size $2 --iterations $3 \
   --batch-sizes $4 --repeats 5 --dtype $5 $6 --out gpurun_out/evidence/sweep_$7 > gpurun_out/evidence/sweep_$7.log 2>&1; echo "sweep $7 rc=$?"; }
+[ "${TRACE_ONLY:-0}" = 1 ] && sweep() { :; }
 H=1,2,4,5,8,10,16,20,25,40,50,80,100,125,200,250,400,500,625,1000,1250,2000
 F=1,2,4,5,8,10,16,20,25,40,50,80,100,125,200,250,400,500
 sweep vector 16384 10000 all f32 "" skeleton

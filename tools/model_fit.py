@@ -68,9 +68,13 @@ def main():
            "Sweeps: `python -m paper_2501_09398_b200 sweep` (5 repeats per K, host wall-clock T_C and T_E as "
            "in the paper; odd K on the ping-pong solvers re-points ONE executable (`IB_FLAG_PATCH`) so T_C "
            "is one K-node graph). Traces: `python -m paper_2501_09398_b200 trace` (CUPTI kernel records + "
-           "host events on the CUPTI clock; t_l from idle-device launches; k_c / b_c a least-squares fit of "
+           "host events on the CUPTI clock; the first two launches of the traced executable, whose nodes "
+           "CUPTI instruments on first launch, are dropped; FDTD's two launches per iteration are one model "
+           "'kernel'; t_l from idle-device launches timed with CUDA events and no profiler attached, the "
+           "CUPTI-timed value beside it; k_c / b_c a least-squares fit of "
            "the whole build time T_C at four batch sizes — the phases fit_creation uses; m_base / m_node a "
-           "fit of the device memory a built graph holds at four sizes). Everything below is computed by "
+           "fit of the device memory a built graph holds at 1000-8000 iterations, where cudaMemGetInfo's "
+           "2 MiB steps resolve it). Everything below is computed by "
            "the reference package itself (`tools/model_fit.py`), unchanged.", "",
            "## Sweep fits (reference `fit_creation` / `fit_execution`, validity filter 0.25 I_k, "
            "`recommend_from_coefficients`)", "",
@@ -117,7 +121,7 @@ def main():
         params_path = os.path.join(d, "params.txt")
         params, memory = parse_params(params_path)
         rows.append(f"| {label} | {t['t_k']*1e6:.2f} | {t['t_i']*1e6:.2f} | {t['t_a']*1e6:.2f} | "
-                    f"{t['t_b']*1e6:.2f} | {t['t_l']*1e6:.2f} | {t['t_l_traced_run']*1e6:.0f} | "
+                    f"{t['t_b']*1e6:.2f} | {t['t_l']*1e6:.2f} | {t.get('t_l_cupti', float('nan'))*1e6:.2f} | "
                     f"{t['k_c']*1e6:.3f} | {t['b_c']*1e6:.1f} | {t['k_c_node_add']*1e6:.2f} | "
                     f"{memory.base_bytes} | {memory.bytes_per_node} |")
         _, rec_txt, _ = ref_cli("optimize", "--params", params_path, "--iterations", str(total))
@@ -156,8 +160,8 @@ def main():
     if rows:
         out += ["## Measured platform constants (`trace`; µs unless stated)", "",
                 "Observation I of the paper (`PAPER.md:208`) holds when t_i < t_a.", "",
-                "| config | t_k | t_i (in-graph gap) | t_a (between graphs) | t_b (stream gap) | t_l (idle launch) | "
-                "t_l of the traced run (queued + CUPTI) | k_c (T_C fit, per iteration) | b_c | node-add interval "
+                "| config | t_k (per iteration) | t_i (in-graph gap) | t_a (between graphs) | t_b (stream gap) | "
+                "t_l (idle launch, no profiler: CUDA events) | t_l (idle launch, CUPTI) | k_c (T_C fit, per iteration) | b_c | node-add interval "
                 "| m_base (B) | m_node (B/iteration) |",
                 "|---|---|---|---|---|---|---|---|---|---|---|---|"] + rows + [""]
         out += ["## `iterbatch optimize` (reference CLI) on the measured params files", "",
