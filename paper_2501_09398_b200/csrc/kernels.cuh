@@ -409,8 +409,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   pdl_wait();  // from here on the previous kernel's writes are visible
   bool halo_stored = false;  // stored into a neighbour's halo plane: fence before retiring
-  auto issue = [&](int t) {
-    const int s = t % nstages;
+  auto issue = [&](int t, int s) {  // plane i0 - 1 + t into stage s
     int q = i0 - 1 + t;
     const bool out_row = (t >= 1 && t <= n_out);
     q = q < qlo ? qlo : (q > qhi ? qhi : q);
@@ -420,8 +419,26 @@ __global__ void __launch_bounds__(256)
       bulk_g2s(ringP + (size_t)s * TM, power + (int64_t)(i0 - 1 + t) * M + m0, bytesP, &bar[s]);
   };
   if (tid == 0)
-    for (int t = 0; t < min(nstages, n_load); ++t) issue(t);
+    for (int t = 0; t < min(nstages, n_load); ++t) issue(t, t);
 
+  // per-group neighbour masks, computed once: the plane loop has no 64-bit division by L
+  bool gok[G], has_ym[G], has_yp[G], has_zl[G], has_zr[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int64_t m = m0 + ((int64_t)g * 256 + tid) * V;
+    gok[g] = m < m1;
+    if (D3) {
+      const int64_t j = m / L, l = m - j * L;
+      has_ym[g] = j > 0;
+      has_yp[g] = j < C - 1;
+      has_zl[g] = l > 0;
+      has_zr[g] = l + V < L;
+    } else {
+      has_ym[g] = has_yp[g] = false;
+      has_zl[g] = m > 0;
+      has_zr[g] = m + V < M;
+    }
+  }
   T up[G][V], cu[G][V];
   // planes t=0 (x-1 of the first output row) and t=1 (first output row) into registers
   mbar_wait(&bar[0], 0);
@@ -437,29 +454,31 @@ __global__ void __launch_bounds__(256)
   __syncthreads();  // stage of t=0 is free
   if (tid == 0 && nstages < n_load) {
     fence_proxy_async();
-    issue(nstages);
+    issue(nstages, 0);
   }
+  // stages of planes tc = u+1 / td = u+2 and td's mbarrier phase, advanced incrementally (no
+  // division by the run-time ring depth in the loop)
+  int sc = 1 % nstages, sd = 2 % nstages;
+  uint32_t phd = (2 / nstages) & 1;
   for (int u = 0; u < n_out; ++u) {
     const int i = i0 + u;
-    const int tc = u + 1, td = u + 2;
-    const T *pc = ringT + (size_t)(tc % nstages) * cap - lo;  // index with global m
-    const T *pd = ringT + (size_t)(td % nstages) * cap - lo;
-    const T *pp = ringP + (size_t)(tc % nstages) * TM - m0;
-    mbar_wait(&bar[td % nstages], (td / nstages) & 1);
+    const int tc = u + 1;
+    const T *pc = ringT + (size_t)sc * cap - lo;  // index with global m
+    const T *pd = ringT + (size_t)sd * cap - lo;
+    const T *pp = ringP + (size_t)sc * TM - m0;
+    mbar_wait(&bar[sd], phd);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int64_t m = m0 + ((int64_t)g * 256 + tid) * V;
-      if (m >= m1) continue;
+      if (!gok[g]) continue;
       T dn[V], ym[V], yp[V], pw[V], out[V];
       ld16<T>(dn, pd + m);
       ld16<T>(pw, pp + m);
       if (D3) {
-        const int j = (int)(m / L);
-        const int l = (int)(m - (int64_t)j * L);
-        if (j > 0) ld16<T>(ym, pc + m - L); else for (int e = 0; e < V; ++e) ym[e] = cu[g][e];
-        if (j < C - 1) ld16<T>(yp, pc + m + L); else for (int e = 0; e < V; ++e) yp[e] = cu[g][e];
-        const T zl = l > 0 ? pc[m - 1] : cu[g][0];
-        const T zr = l + V < L ? pc[m + V] : cu[g][V - 1];
+        if (has_ym[g]) ld16<T>(ym, pc + m - L); else for (int e = 0; e < V; ++e) ym[e] = cu[g][e];
+        if (has_yp[g]) ld16<T>(yp, pc + m + L); else for (int e = 0; e < V; ++e) yp[e] = cu[g][e];
+        const T zl = has_zl[g] ? pc[m - 1] : cu[g][0];
+        const T zr = has_zr[g] ? pc[m + V] : cu[g][V - 1];
 #pragma unroll
         for (int e = 0; e < V; ++e) {
           const T zm = e > 0 ? cu[g][e - 1] : zl;
@@ -467,8 +486,8 @@ __global__ void __launch_bounds__(256)
           out[e] = hotspot_cell<T, true>(up[g][e], cu[g][e], dn[e], ym[e], yp[e], zm, zp, pw[e], k, loss);
         }
       } else {
-        const T yl = m > 0 ? pc[m - 1] : cu[g][0];
-        const T yr = m + V < M ? pc[m + V] : cu[g][V - 1];
+        const T yl = has_zl[g] ? pc[m - 1] : cu[g][0];
+        const T yr = has_zr[g] ? pc[m + V] : cu[g][V - 1];
 #pragma unroll
         for (int e = 0; e < V; ++e) {
           const T a = e > 0 ? cu[g][e - 1] : yl;
@@ -496,8 +515,11 @@ __global__ void __launch_bounds__(256)
     const int tn = tc + nstages;
     if (tid == 0 && tn < n_load) {
       fence_proxy_async();
-      issue(tn);
+      issue(tn, sc);  // tn and tc share a stage
     }
+    sc = sd;
+    sd = sd + 1 == nstages ? 0 : sd + 1;
+    if (sd == 0) phd ^= 1u;
   }
   if (fence_sys && halo_stored) peer_fence();
 }
@@ -720,8 +742,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
     const uint32_t ebytes = (uint32_t)((ehi - elo + 1) * P * sizeof(T));
     const uint32_t hbytes = (uint32_t)((hhi - elo + 1) * P * sizeof(T));
     const int erow0 = elo - (j0 - 1);  // ring row of lattice row elo
-    auto issue = [&](int t) {
-      const int s = (int)((g_base + t) % nstages);
+    auto issue = [&](int t, int s) {  // plane ib + t into stage s
       const int p = ib + t;
       const bool h = p < i1;
       T *st = ring + (size_t)s * stage;
@@ -736,8 +757,12 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
     __syncthreads();  // every thread is done with the previous run's stages
     if (tid == 0) {
       fence_proxy_async();
-      for (int t = 0; t < min(nstages, nload); ++t) issue(t);
+      for (int t = 0; t < min(nstages, nload); ++t) issue(t, (int)((g_base + t) % nstages));
     }
+    // stage and mbarrier phase of use g_base + t, advanced incrementally: no integer division by
+    // the run-time ring depth in the plane loop (each costs ~25 uniform instructions per warp)
+    int sc = (int)(g_base % nstages), sp = 0;
+    uint32_t pc = (g_base / nstages) & 1;
     const int jj = j0 - 1 + r;  // this thread's lattice row
     const bool row_ok = r <= h && jj >= 0 && jj <= ny;
     const bool jlt = jj < ny, jin = jj >= 1 && jj < ny;
@@ -747,12 +772,13 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
     for (int i = ib; i < i1; ++i) {
       const int t = i - ib;
       const bool write = i >= i0;
-      const uint32_t gs = g_base + t;
-      if (t == 0 || MODE == kLfE) mbar_wait(&bar[gs % nstages], (gs / nstages) & 1);
-      if (MODE != kLfE && t + 1 < nload) mbar_wait(&bar[(gs + 1) % nstages], ((gs + 1) / nstages) & 1);
-      const T *Ec = ring + (size_t)(gs % nstages) * stage + r * P + k0;  // E_old(i), my row/group
-      const T *En = ring + (size_t)((gs + 1) % nstages) * stage + r * P + k0;  // E_old(i+1)
-      T *Hr = ring + (size_t)(gs % nstages) * stage + 3 * ER * P + r * P + k0;  // H(i), my row/group
+      const int sn = sc + 1 == nstages ? 0 : sc + 1;
+      const uint32_t pn = sn == 0 ? pc ^ 1u : pc;
+      if (t == 0 || MODE == kLfE) mbar_wait(&bar[sc], pc);
+      if (MODE != kLfE && t + 1 < nload) mbar_wait(&bar[sn], pn);
+      const T *Ec = ring + (size_t)sc * stage + r * P + k0;  // E_old(i), my row/group
+      const T *En = ring + (size_t)sn * stage + r * P + k0;  // E_old(i+1)
+      T *Hr = ring + (size_t)sc * stage + 3 * ER * P + r * P + k0;  // H(i), my row/group
       const bool ilt = i < nx, iin = i >= 1 && i < nx;
       T exr[V], eyr[V], ezr[V], hx[V], hy[V], hz[V];
       // ---- phase H --------------------------------------------------------------------------
@@ -815,7 +841,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
       __syncthreads();  // H_new(i) complete in the ring; plane t-1's stage is free
       if (tid == 0 && t >= 1 && t - 1 + nstages < nload) {
         fence_proxy_async();
-        issue(t - 1 + nstages);
+        issue(t - 1 + nstages, sp);  // plane t-1's stage
       }
       // ---- phase E (owned rows) ---------------------------------------------------------------
       if (MODE != kLfH && row_ok && r >= 1) {
@@ -860,6 +886,9 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
           hz_prev[e] = hz[e];
         }
       }
+      sp = sc;
+      sc = sn;
+      pc = pn;
     }
     g_base += (uint32_t)nload;
   }

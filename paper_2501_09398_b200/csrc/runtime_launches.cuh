@@ -36,7 +36,9 @@ int tma_groups(const ib_ctx *c) {  // G such that TM = G*V*256 holds whole y-row
   constexpr int V = 16 / sizeof(T);
   const bool d3 = c->solver == IB_SOLVER_HOTSPOT3D;
   const int64_t L = d3 ? c->dims[2] : 1;
+  const int64_t force = env_int("IB_TMA_GROUPS", 0);  // tuning: 1, 2 or 4 groups per thread
   for (int G : {2, 1, 4}) {
+    if (force > 0 && G != force) continue;
     const int64_t TM = (int64_t)G * V * 256;
     if (!d3 || (TM % L == 0 && L <= 1024)) return G;
   }
@@ -156,7 +158,12 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         const bool wide3d = d3 && threads_per_row * rows >= (1LL << 19) && threads_per_row % 32 == 0 &&
                             32 % (L / V) == 0 &&
                             ((threads_per_row + 127) / 128) * ((rows + 31) / 32) <= c->num_sms;
-        int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? (wide3d ? 1024 : 256) : 512);
+        // binary64 3-D (two cells per 16-byte group, so twice the threads of binary32 for a grid):
+        // 4 rows per thread in 128-thread CTAs measured best — Hotspot3D 512^2x8 6.57 us/iter
+        // against 7.31 for the 256-thread / R = 2 binary32 default, 6.70-6.72 for R = 4 / 256 and
+        // R = 2 / 128 (tools/hotspot_tune.py, DTYPE=f64, graph with PDL edges)
+        const bool d3_f64 = d3 && sizeof(T) == 8 && !wide3d;
+        int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? (wide3d ? 1024 : (d3_f64 ? 128 : 256)) : 512);
         bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
         const int64_t bx_max = std::max<int64_t>(32, env_int("IB_HOTSPOT_BX", wide3d ? 128 : 256) / 32 * 32);  // CTA width cap
         const int64_t bx = std::min<int64_t>(std::min<int64_t>(bx_max, bs), (threads_per_row + 31) / 32 * 32);
@@ -177,7 +184,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", 1);
         if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
         if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
-        if (wide3d && sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 4) R = 4;
+        if ((wide3d || d3_f64) && sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 4) R = 4;
         // 2-D grids past one wave of the 256 x 2 / R = 2 shape (two 512-thread CTAs per SM at 49
         // registers): one row per thread (~30 registers, four CTAs per SM) measured faster —
         // 2048^2 7.89 vs 8.67 us/iter, 1536^2 5.92 vs 6.75 (tools/hotspot2d_shapes.py)

@@ -6,9 +6,12 @@ from paper_2501_09398_b200 import cli, workloads as wl
 KEYS = ("IB_HOTSPOT_KERNEL", "IB_HOTSPOT_VEC_ROWS", "IB_HOTSPOT_RPC", "IB_TMA_STAGES", "IB_HOTSPOT_BLOCK",
         "IB_VECTOR_BLOCK", "IB_HOTSPOT_SHUFFLE")
 cfgs = [("hotspot3d", [512, 8], 1000), ("hotspot2d", [1024], 2000)]
+if os.environ.get("CFGS"):  # e.g. CFGS=hotspot2d
+    cfgs = [c for c in cfgs if c[0] in os.environ["CFGS"].split(",")]
+DTYPE = os.environ.get("DTYPE", "f32")
 variants = [("auto", {})]
 for r in (1, 2, 4):
-    for bs in (128, 256, 512):
+    for bs in (128, 256, 512, 1024):
         variants.append((f"vec R={r} sh=1 block={bs}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
                                                         "IB_HOTSPOT_SHUFFLE": 1, "IB_HOTSPOT_BLOCK": bs}))
 
@@ -24,7 +27,7 @@ for w, size, n in cfgs:
         for k in KEYS:
             os.environ.pop(k, None)
         os.environ.update({k: str(v) for k, v in env.items()})
-        s = wl.DeviceSolver(st, "f32")
+        s = wl.DeviceSolver(st, DTYPE)
         s.run_batched(50, n // 50, pdl=True)
         g, gp, sp = [], [], []
         for _ in range(5):
@@ -35,6 +38,6 @@ for w, size, n in cfgs:
             s.flush_l2(); s.upload(st)
             sp.append(s.run_stream(n).gpu_s / n)
         m = lambda x: 1e6 * statistics.median(x)
-        print(f"{w:9s} {name:16s} graph {m(g):6.3f}  graph+pdl {m(gp):6.3f}  stream {m(sp):6.3f}  "
+        print(f"{DTYPE} {w:9s} {name:24s} graph {m(g):6.3f}  graph+pdl {m(gp):6.3f}  stream {m(sp):6.3f}  "
               f"ratio {statistics.median(sp)/min(statistics.median(g), statistics.median(gp)):.3f}", flush=True)
         s.close()

@@ -40,6 +40,27 @@ __global__ void k_scale(const float4 *a, float4 *b, const float4 *, int n) {
   b[i] = make_float4((float)(v.x * c), (float)(v.y * c), (float)(v.z * c), (float)(v.w * c));
 }
 
+// binary64 Hotspot2D 1024^2 pattern: double2 per thread (512 per 1024-double row), three row reads
+// + power + write; RB rows per thread (RB+2 row reads for RB outputs)
+template <int RB>
+__global__ void k_rows64(const double2 *a, double2 *b, const double2 *p, int n) {
+  pdl();
+  const int row = 512, i0 = (blockIdx.x * blockDim.x + threadIdx.x);
+  const int x = i0 % row, r0 = (i0 / row) * RB;
+  double2 v[RB + 2];
+#pragma unroll
+  for (int q = 0; q < RB + 2; ++q) {
+    int r = r0 - 1 + q;
+    r = r < 0 ? 0 : (r > 1023 ? 1023 : r);
+    v[q] = a[r * row + x];
+  }
+#pragma unroll
+  for (int q = 0; q < RB; ++q) {
+    const double2 w = p[(r0 + q) * row + x];
+    b[(r0 + q) * row + x] = make_double2(v[q].x + v[q + 1].x + v[q + 2].x + w.x, v[q].y + v[q + 1].y + v[q + 2].y + w.y);
+  }
+}
+
 int main() {
   const int n = 1024 * 1024 / 4, K = 100, reps = 20;
   float4 *a, *b, *p;
@@ -131,6 +152,47 @@ int main() {
       cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       printf("%-32s pdl=1  %.3f us/launch\n", sn[f], 1000.f * ms / (reps * K));
+      cudaGraphExecDestroy(ge); cudaGraphDestroy(g);
+    }
+  }
+  // binary64 Hotspot2D 1024^2 access pattern (no arithmetic beyond the adds): the floor the
+  // binary64 k_hotspot_vec runs against
+  {
+    const int n2 = 1024 * 1024 / 2;
+    double2 *a2, *b2, *p2;
+    cudaMalloc(&a2, n2 * 16); cudaMalloc(&b2, n2 * 16); cudaMalloc(&p2, n2 * 16);
+    cudaMemset(a2, 0, n2 * 16); cudaMemset(b2, 0, n2 * 16); cudaMemset(p2, 0, n2 * 16);
+    struct { const char *name; void (*fn)(const double2 *, double2 *, const double2 *, int); int rb, block; } v[] = {
+        {"f64 3 rows + power + write, R=1, 256 thr", k_rows64<1>, 1, 256},
+        {"f64 3 rows + power + write, R=1, 512 thr", k_rows64<1>, 1, 512},
+        {"f64 4 rows + 2 power + 2 writes, R=2, 256", k_rows64<2>, 2, 256},
+        {"f64 R=2, 512 thr", k_rows64<2>, 2, 512},
+        {"f64 R=4, 256 thr", k_rows64<4>, 4, 256},
+        {"f64 R=4, 128 thr", k_rows64<4>, 4, 128}};
+    for (auto &c : v) {
+      cudaGraph_t g; cudaGraphExec_t ge;
+      cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+      for (int k = 0; k < K; ++k) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n2 / c.rb / c.block); cfg.blockDim = dim3(c.block); cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at; cfg.numAttrs = k > 0 ? 1 : 0;
+        const double2 *src = (k & 1) ? b2 : a2; double2 *dst = (k & 1) ? a2 : b2;
+        cudaLaunchKernelEx(&cfg, c.fn, src, dst, (const double2 *)p2, n2);
+      }
+      cudaStreamEndCapture(s, &g);
+      cudaGraphInstantiate(&ge, g, 0);
+      cudaGraphUpload(ge, s);
+      cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+      cudaGraphLaunch(ge, s);
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("%-44s pdl=1  %.3f us/launch\n", c.name, 1000.f * ms / (reps * K));
       cudaGraphExecDestroy(ge); cudaGraphDestroy(g);
     }
   }

@@ -82,17 +82,17 @@ def main():
     a = ap.parse_args()
     lines = [f"# ncu summary ({a.round})", "",
              "`ncu --set full --clock-control none --import-source on` of `tools/profile_run.py` "
-             "(stream mode, binary32, the BASELINE configs), via `tools/profile_all.sh`. Times are "
+             "(stream mode, binary64 and binary32, the BASELINE configs), via `tools/profile_all.sh`. Times are "
              "cold-cache, serialised replays (compare shares, not absolutes); DRAM bytes are per launch.",
              "",
-             "| config | kernel | grid x block | regs | time (us) | DRAM read (MB) | DRAM write (MB) | "
+             "| config | dtype | kernel | grid x block | regs | time (us) | DRAM read (MB) | DRAM write (MB) | "
              "DRAM % peak | L2 hit % | L1 hit % | SM % | warps active % | inst (M) |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = {}
-    for rep, key in REPORTS.items():
-        path = os.path.join(a.dir, f"ncu_{rep}_raw.csv")
+    for (rep, key), dtype in [(kv, dt) for dt in ("f64", "f32") for kv in REPORTS.items()]:
+        path = os.path.join(a.dir, f"ncu_{rep}_{dtype}_raw.csv")
         if not os.path.exists(path):
-            path = os.path.join(a.dir, f"ncu_{rep}.ncu-rep")
+            path = os.path.join(a.dir, f"ncu_{rep}_{dtype}.ncu-rep")
         if not os.path.exists(path):
             continue
         per_kernel = {}
@@ -102,7 +102,7 @@ def main():
             rd = scaled(e, "dram__bytes_read.sum", 1e6)
             wr = scaled(e, "dram__bytes_write.sum", 1e6)
             lines.append(
-                f"| {key} | `{name}` | {int(e['launch__grid_size'][0])} x {int(e['launch__block_size'][0])} | "
+                f"| {key} | {dtype} | `{name}` | {int(e['launch__grid_size'][0])} x {int(e['launch__block_size'][0])} | "
                 f"{int(e['launch__registers_per_thread'][0])} | {t_us:.2f} | {rd:.2f} | {wr:.2f} | "
                 f"{e['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'][0]:.1f} | "
                 f"{e['lts__t_sector_hit_rate.pct'][0]:.1f} | {e['l1tex__t_sector_hit_rate.pct'][0]:.1f} | "
@@ -111,7 +111,7 @@ def main():
                 f"{e['smsp__inst_executed.sum'][0] / 1e6:.2f} |")
             per_kernel.setdefault(name, []).append((rd + wr) * 1e6)
         # bytes per iteration = sum over the iteration's kernels of their mean per-launch traffic
-        traffic[key] = int(sum(sum(v) / len(v) for v in per_kernel.values()))
+        traffic[f"{key}:{dtype}"] = int(sum(sum(v) / len(v) for v in per_kernel.values()))
     if a.launches and os.path.exists(a.launches):
         lines += ["", "## Launch list of a short bench run (`ncu --metrics gpu__time_duration.sum`)", ""]
         shares = {}

@@ -14,12 +14,14 @@ full() {  # name regex skip -- profile_run.py args
   ncu -i "gpurun_out/ncu_$name.ncu-rep" --page raw --csv > "gpurun_out/ncu_${name}_raw.csv" 2>/dev/null
   [ "${KEEP_REPS:-0}" = 1 ] || rm -f "gpurun_out/ncu_$name.ncu-rep"
 }
-full hotspot2d k_hotspot 2 --workload hotspot2d --size 1024 --iters 4
-full hotspot3d_512 k_hotspot 2 --workload hotspot3d --size 512,8 --iters 4
-full hotspot3d_large k_hotspot 2 --workload hotspot3d --size 2048,2048,256 --iters 4
-full fdtd k_fdtd 2 --workload fdtd --size 256 --iters 3
-full fdtd_fused k_fdtd_lf 2 --workload fdtd --size 256 --iters 4 --fuse
-full skeleton k_vector 2 --workload vector --size 16384 --iters 4
+for dt in f64 f32; do
+  full hotspot2d_$dt k_hotspot 2 --workload hotspot2d --size 1024 --iters 4 --dtype $dt
+  full hotspot3d_512_$dt k_hotspot 2 --workload hotspot3d --size 512,8 --iters 4 --dtype $dt
+  full hotspot3d_large_$dt k_hotspot 2 --workload hotspot3d --size 2048,2048,256 --iters 4 --dtype $dt
+  full fdtd_$dt k_fdtd 2 --workload fdtd --size 256 --iters 3 --dtype $dt
+  full fdtd_fused_$dt k_fdtd_lf 2 --workload fdtd --size 256 --iters 4 --fuse --dtype $dt
+  full skeleton_$dt k_vector 2 --workload vector --size 16384 --iters 4 --dtype $dt
+done
 # launch list of a short bench run (cold-cache, serialised; compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 3 --quick \
