@@ -122,7 +122,7 @@ def test_params_file_drives_the_reference_optimizer():
     code, out, err = _cli("simulate", "--params", path, "--iterations", "200", "--batch-size", str(k_star))
     assert code == 0, err
     creation, execution, total = (float(x) for x in out.split(","))
-    assert creation > 0 and execution > 0 and abs(total - creation - execution) < 1e-9
+    assert creation > 0 and execution > 0 and abs(total - creation - execution) < 3e-9  # 9-decimal output
 
 
 def test_writers_emit_the_reference_schema(tmp_path):
