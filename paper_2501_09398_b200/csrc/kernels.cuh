@@ -759,8 +759,12 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
       fence_proxy_async();
       for (int t = 0; t < min(nstages, nload); ++t) issue(t, (int)((g_base + t) % nstages));
     }
-    // stage and mbarrier phase of use g_base + t, advanced incrementally: no integer division by
-    // the run-time ring depth in the plane loop (each costs ~25 uniform instructions per warp)
+    // stage and mbarrier phase of use g_base + t. binary64: advanced incrementally, no integer
+    // division by the run-time ring depth in the plane loop (each costs ~25 uniform instructions
+    // per warp): fused 288 -> 266-275 us/iter, two half-steps 384-395 -> 377-380 at 256^3.
+    // binary32 keeps the division form, measured faster there on 3 of 4 fresh boxes (fused
+    // 132-138 vs 131-146 us/iter, two half-steps 193-195 vs 196-201).
+    constexpr bool INCR = sizeof(T) == 8;
     int sc = (int)(g_base % nstages), sp = 0;
     uint32_t pc = (g_base / nstages) & 1;
     const int jj = j0 - 1 + r;  // this thread's lattice row
@@ -772,8 +776,13 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
     for (int i = ib; i < i1; ++i) {
       const int t = i - ib;
       const bool write = i >= i0;
-      const int sn = sc + 1 == nstages ? 0 : sc + 1;
-      const uint32_t pn = sn == 0 ? pc ^ 1u : pc;
+      if (!INCR) {
+        const uint32_t gs = g_base + t;
+        sc = (int)(gs % nstages);
+        pc = (gs / nstages) & 1;
+      }
+      const int sn = INCR ? (sc + 1 == nstages ? 0 : sc + 1) : (int)((g_base + t + 1) % nstages);
+      const uint32_t pn = INCR ? (sn == 0 ? pc ^ 1u : pc) : ((g_base + t + 1) / nstages) & 1;
       if (t == 0 || MODE == kLfE) mbar_wait(&bar[sc], pc);
       if (MODE != kLfE && t + 1 < nload) mbar_wait(&bar[sn], pn);
       const T *Ec = ring + (size_t)sc * stage + r * P + k0;  // E_old(i), my row/group
@@ -841,7 +850,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
       __syncthreads();  // H_new(i) complete in the ring; plane t-1's stage is free
       if (tid == 0 && t >= 1 && t - 1 + nstages < nload) {
         fence_proxy_async();
-        issue(t - 1 + nstages, sp);  // plane t-1's stage
+        issue(t - 1 + nstages, INCR ? sp : (int)((g_base + t - 1 + nstages) % nstages));  // plane t-1's stage
       }
       // ---- phase E (owned rows) ---------------------------------------------------------------
       if (MODE != kLfH && row_ok && r >= 1) {

@@ -20,6 +20,8 @@ if os.environ.get("ALL"):
         variants.append((f"tma rpc={rpc}", {"IB_HOTSPOT_KERNEL": "tma", "IB_HOTSPOT_RPC": rpc}))
     for rpc in (2, 4, 8):
         variants.append((f"scalar rpc={rpc}", {"IB_HOTSPOT_KERNEL": "scalar", "IB_HOTSPOT_RPC": rpc}))
+if os.environ.get("AUTO_ONLY"):
+    variants = variants[:1]
 vec_variants = [(f"block={bs}", {"IB_VECTOR_BLOCK": bs}) for bs in (128, 256, 512, 1024)]
 for w, size, n in cfgs:
     st = cli.build_workload(w, size)

@@ -14,6 +14,7 @@ for tool in memcheck racecheck; do
   san $tool hotspot2d 64,48 f32; san $tool hotspot2d 40,128 f32; san $tool hotspot3d 24,20,8 f64
   san $tool hotspot3d 24,16,8 f32; san $tool hotspot3d 24,16,8 f64  # warp-shuffle paths
   KTAG=tma IB_HOTSPOT_KERNEL=tma san $tool hotspot3d 40,16,256 f32
+  KTAG=tma IB_HOTSPOT_KERNEL=tma san $tool hotspot3d 40,16,256 f64; san $tool hotspot3d 24,64,8 f64
   KTAG=scalar IB_HOTSPOT_KERNEL=scalar san $tool hotspot2d 40,128 f32
   san $tool fdtd 9,5,7 f32; san $tool fdtd 20,17,40 f64; KTAG=lean IB_FDTD_KERNEL=lean san $tool fdtd 9,5,7 f32
   san $tool fdtd 9,5,7 f32 --fuse; san $tool fdtd 20,17,40 f64 --fuse
@@ -24,6 +25,7 @@ for tool in memcheck racecheck; do
 done
 san synccheck hotspot2d 40,128 f32; san synccheck fdtd 20,17,40 f32 --fuse; san synccheck fdtd 20,17,40 f32
 KTAG=tma IB_HOTSPOT_KERNEL=tma san synccheck hotspot3d 40,16,256 f32
+KTAG=tma IB_HOTSPOT_KERNEL=tma san synccheck hotspot3d 40,16,256 f64; san synccheck fdtd 20,17,40 f64 --fuse
 {
   echo "| run (tool_workload_size_dtype[_flags][_kernel]) | summary |"
   echo "|---|---|"
