@@ -414,8 +414,8 @@ def measure_ours(name, cfg, dtype, args, dist: Dist, device: int, headline: bool
             roof["limit"] = "per-launch floor"
             roof["note"] += ("; the state (%.1f MB) stays L2-resident across iterations (ncu: ~0 DRAM bytes per "
                              "launch in steady state), so the binding limit is the per-launch floor of a "
-                             "PDL-chained one-wave kernel with this access pattern, not HBM (DESIGN.md §4, "
-                             "profiles/r01_microbench_floor.txt)" % (state_bytes / 1e6))
+                             "PDL-chained launch with this access pattern plus its arithmetic, not HBM "
+                             "(DESIGN.md §4 and §10, profiles/r02_microbench_floor.txt)" % (state_bytes / 1e6))
         out = {
             "name": name, "dtype": dtype, "workload": cfg["label"], "iterations": n, "batch_size": k, "pdl": pdl,
             "us_per_iter": 1e6 * step_mean / n, "ms_per_step": 1e3 * step_mean, "steps": steps,

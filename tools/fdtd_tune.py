@@ -9,7 +9,7 @@ dtype = os.environ.get("DTYPE", "f32")
 st = cli.build_workload("fdtd", [n])
 variants = [("two-kernel staged (default)", False, {}), ("two-kernel lean", False, {"IB_FDTD_KERNEL": "lean"}),
             ("fused default", True, {})]
-shapes = ((4, 6), (3, 7), (3, 8), (2, 8), (2, 10), (1, 12)) if dtype == "f32" else ((4, 3), (3, 4), (2, 5), (2, 6), (1, 6))
+shapes = ((4, 3), (4, 4), (4, 5), (4, 6), (3, 4), (3, 7), (3, 8), (2, 8), (2, 10)) if dtype == "f32" else ((4, 3), (3, 4), (2, 3), (2, 4), (2, 5), (2, 6), (1, 6))
 for fuse in (True, False):
     for tj, ns in shapes:
         variants.append((f"{'fused' if fuse else 'two-kernel'} tj={tj} ns={ns}", fuse,
