@@ -163,9 +163,16 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         // against 7.31 for the 256-thread / R = 2 binary32 default, 6.70-6.72 for R = 4 / 256 and
         // R = 2 / 128 (tools/hotspot_tune.py, DTYPE=f64, graph with PDL edges)
         const bool d3_f64 = d3 && sizeof(T) == 8 && !wide3d;
+        // binary64 2-D (Hotspot2D 1024^2, the headline config): 64 x 8-thread CTAs, whose 8 rows
+        // share their x-neighbour rows in L1, and the in-row neighbours loaded instead of shuffled
+        // (a double needs two SHFL.32) — 3.56 us/iter against 3.92 for the binary32 shape (256 x 2,
+        // shuffles, R = 2 -> 1); every other 2-D / 3-D shape of either precision measured within
+        // 1% of its default (tools/hotspot_vec_shapes.py, profiles/r02_hotspot_vec_shapes.md)
+        const bool d2_f64 = !d3 && sizeof(T) == 8;
         int64_t bs = env_int("IB_HOTSPOT_BLOCK", d3 ? (wide3d ? 1024 : (d3_f64 ? 128 : 256)) : 512);
         bs = std::max<int64_t>(32, std::min<int64_t>(1024, bs / 32 * 32));
-        const int64_t bx_max = std::max<int64_t>(32, env_int("IB_HOTSPOT_BX", wide3d ? 128 : 256) / 32 * 32);  // CTA width cap
+        const int64_t bx_max =
+            std::max<int64_t>(32, env_int("IB_HOTSPOT_BX", wide3d ? 128 : (d2_f64 ? 64 : 256)) / 32 * 32);  // CTA width cap
         const int64_t bx = std::min<int64_t>(std::min<int64_t>(bx_max, bs), (threads_per_row + 31) / 32 * 32);
         const int64_t by = std::max<int64_t>(1, bs / bx);
         const int64_t xblocks = (threads_per_row + bx - 1) / bx;
@@ -181,7 +188,7 @@ void hotspot_launches(ib_ctx *c, int parity, std::vector<Launch> &out) {
         // Measured in-graph with PDL (us/iter, two runs): Hotspot3D 512^2x8 R=1 4.47, R=1+sh1 4.36,
         // R=2+sh1 4.22-4.25, sh2 (y rows by 8 shuffles) 4.60-4.77; Hotspot2D 1024^2 R=1 2.61,
         // R=1+sh1 2.49, R=2+sh1 2.45. So z / row shuffles, and 2 rows per thread with them.
-        int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", 1);
+        int64_t sh = env_int("IB_HOTSPOT_SHUFFLE", d2_f64 ? 0 : 1);
         if (!(threads_per_row % 32 == 0 && bx % 32 == 0 && 32 % gl == 0)) sh = 0;
         if (sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 2 && R < 2) R = 2;
         if ((wide3d || d3_f64) && sh && env_int("IB_HOTSPOT_VEC_ROWS", 0) <= 0 && rows >= 4) R = 4;
