@@ -1,5 +1,5 @@
 """Graph-mode variants on B200: build cost and execution per iteration for every way the runtime
-can batch iterations (run under gpurun; writes gpurun_out/graph_modes.json and prints a table).
+can batch iterations (run under gpurun; writes gpurun_out/graph_modes_<dtype>.json, DTYPE=f32|f64 and prints a table).
 
   stream            Listing 1: one cudaLaunchKernel per kernel from the C++ loop
   stream+pdl        the same with the programmatic-stream-serialization launch attribute
@@ -24,6 +24,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl  # noqa: E402
 
+DTYPE = os.environ.get("DTYPE", "f32")
 CFGS = [("skeleton 2^14", "vector", [16384], 10000, 100), ("hotspot2d 1024^2", "hotspot2d", [1024], 10000, 80),
         ("hotspot3d 512^2x8", "hotspot3d", [512, 8], 1000, 40), ("fdtd 256^3", "fdtd", [256], 200, 20)]
 
@@ -32,7 +33,7 @@ def main():
     rows = []
     for label, w, size, n, k in CFGS:
         st = cli.build_workload(w, size)
-        s = wl.DeviceSolver(st, "f32")
+        s = wl.DeviceSolver(st, DTYPE)
 
         def timed(fn):
             xs, tcs = [], []
@@ -85,7 +86,7 @@ def main():
                   flush=True)
         s.close()
     os.makedirs("gpurun_out", exist_ok=True)
-    with open(os.path.join("gpurun_out", "graph_modes.json"), "w") as fh:
+    with open(os.path.join("gpurun_out", f"graph_modes_{DTYPE}.json"), "w") as fh:
         json.dump(rows, fh, indent=1)
 
 

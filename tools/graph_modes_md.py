@@ -5,7 +5,11 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
-rows = json.load(open(os.path.join(ROOT, "gpurun_out", "graph_modes.json")))
+rows = []
+for dt in ("f64", "f32"):
+    path = os.path.join(ROOT, "gpurun_out", f"graph_modes_{dt}.json")
+    if os.path.exists(path):
+        rows += [dict(r, config=f"{r['config']} {dt}") for r in json.load(open(path))]
 cfgs, modes = [], []
 for r in rows:
     if r["config"] not in cfgs:
@@ -13,7 +17,7 @@ for r in rows:
     if r["mode"] not in modes:
         modes.append(r["mode"])
 out = [f"# Graph-mode variants on one B200 ({rnd})", "",
-       "`python tools/graph_modes.py` under gpurun: binary32, device time (CUDA events) per iteration, "
+       "`python tools/graph_modes.py` under gpurun (DTYPE=f64 and f32): device time (CUDA events) per iteration, "
        "L2 flushed before every run, median of 5 runs; T_C = host build time (create + instantiate + "
        "upload), µs. `stream` is Listing 1 (the paper's baseline); `manual` / `capture` are Listing 3 "
        "built with explicit nodes or stream capture; `+pdl` adds programmatic dependent-launch edges "
