@@ -366,9 +366,15 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   // The staged kernel marches planes serially per CTA; while the lattice sits in L2 the fully
   // parallel lean kernels finish sooner (measured us/iter, staged vs lean: 32^3 6.8 / 5.1, 64^3
   // 8.3 / 7.8, 96^3 17.3 / 15.1, 128^3 28.0 / 28.2, 160^3 66.7 / 71.5). IB_FDTD_KERNEL=lean|staged.
+  // Long z rows leave the staged kernel only 1-row tiles or a 3-stage ring (binary64 384^3: TJ=1 /
+  // NS=4 2,508 us/iter, TJ=2 / NS=3 2,042, against 1,408 for the lean kernels: 0.90 of the copy
+  // peak; profiles/r02_size_sweep.md, tools/fdtd_tune.py) — the lean kernels take those shapes too.
   const char *force = env_str("IB_FDTD_KERNEL");
   const int64_t lattice_bytes = 6 * c->lat_fs * c->esize;
-  const bool lean = (force && !std::strcmp(force, "lean")) || lf_config(c).tj == 0 ||
+  const LfConfig cfg = lf_config(c);
+  const bool shallow = cfg.tj <= 1 || cfg.ns <= 3;
+  const bool lean = (force && !std::strcmp(force, "lean")) || cfg.tj == 0 ||
+                    (!force && shallow && env_int("IB_FDTD_TJ", 0) <= 0 && env_int("IB_FDTD_STAGES", 0) <= 0) ||
                     (!force && c->slabs.size() == 1 && !c->dist() && lattice_bytes < (40LL << 20));
   const int nx = (int)c->dims[0];
   const int P = (int)c->slabs.size();
