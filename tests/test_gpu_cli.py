@@ -141,3 +141,38 @@ def test_while_loop_odd_k_many_batches(gpu, workload, size, k, batches):
         s.run_graph(batches)  # the parity moved by `batches`: the run continues on the right buffer
         want2 = wl.state_checksum(wl.run_loop(prog, state, 2 * k * batches, fuse=fuse))
         assert wl.state_checksum(s.download(state)) == want2
+
+
+# ---- the `trace` command: measured model constants for `iterbatch optimize` -------------------------
+@pytest.mark.parametrize("workload,size,kpi", [("hotspot2d", "256", 1), ("fdtd", "16", 2)])
+def test_trace_command_writes_the_measured_model(gpu, capsys, tmp_path, workload, size, kpi):
+    """`trace` end to end: the graph trace holds exactly the traced run (the two CUPTI warm-up
+    launches dropped, batches renumbered from 0), the params file carries every key the reference
+    parser reads (fileio.py:70-125) with t_l measured without a profiler and m_node from graph
+    memory, and FDTD's two launches per iteration make one model 'kernel' (t_k per iteration)."""
+    out = tmp_path / "tr"
+    code, stdout, err = _run_cli(capsys, "trace", "--workload", workload, "--size", size, "--iterations", "200",
+                                 "--batch-size", "20", "--out", str(out))
+    assert code == 0, err
+    import json
+
+    rep = json.loads(stdout.strip().splitlines()[-1])
+    keys = {}
+    for line in (out / "params.txt").read_text().splitlines():
+        if "=" in line and not line.startswith("#"):
+            k, v = line.split("=")
+            keys[k.strip()] = float(v)
+    assert list(keys) == ["t_k", "t_i", "t_a", "t_l", "t_b", "k_c", "b_c", "m_base", "m_node"]
+    assert 0 < keys["t_k"] < 1e-3 and 0 < keys["t_l"] < 1e-3 and keys["k_c"] > 0
+    assert keys["m_node"] > 0  # a kernel node holds ~2.4 KB of device memory per iteration
+    assert rep["t_l_cupti"] > 0 and len(rep["memory_points"]) == 4
+    rows = list(csv.reader(open(out / "graph_trace.csv")))[2:]
+    kinds = [r[1] for r in rows]
+    assert kinds.count("kernel_started") == kinds.count("kernel_ended") == 200 * kpi
+    launched = [int(r[2]) for r in rows if r[1] == "graph_launched"]
+    assert launched == list(range(10))  # 200 / 20 batches, the warm-up launches dropped
+    ts = [float(r[0]) for r in rows]
+    assert ts == sorted(ts)
+    if kpi == 2:  # one model 'kernel' = one iteration = the H and the E launch
+        one = [float(r[0]) for r in rows if r[1] in ("kernel_started", "kernel_ended")]
+        assert keys["t_k"] > 0.5 * (one[3] - one[0])
