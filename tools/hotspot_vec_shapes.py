@@ -17,7 +17,11 @@ workload = "hotspot2d" if len(size) == 1 else "hotspot3d"
 st = cli.build_workload(workload, size)
 RS = (1, 2) if workload == "hotspot2d" else (1, 2, 4)
 shapes = [("auto", {})]
-for r, bs, bx, sh in itertools.product(RS, (128, 256, 512, 1024), (64, 128, 256), (0, 1)):
+BXS = tuple(int(x) for x in os.environ.get("BXS", "64,128,256").split(","))
+SHS = tuple(int(x) for x in os.environ.get("SHS", "0,1").split(","))
+if os.environ.get("RS"):
+    RS = tuple(int(x) for x in os.environ["RS"].split(","))
+for r, bs, bx, sh in itertools.product(RS, (128, 256, 512, 1024), BXS, SHS):
     if bx > bs:
         continue
     shapes.append((f"R={r} block={bs} bx={bx} sh={sh}", {"IB_HOTSPOT_KERNEL": "vec", "IB_HOTSPOT_VEC_ROWS": r,
