@@ -70,12 +70,15 @@ def test_hotspot_tma_chunking_and_ring_depth(gpu, env, rpc, stages):
         assert np.array_equal(np.asarray(got, np.float32), want), shape
 
 
+@pytest.mark.parametrize("bx", [32, 256])
 @pytest.mark.parametrize("shuffle", [0, 1, 2])
 @pytest.mark.parametrize("rows,block", [(1, 256), (2, 256), (4, 256), (1, 1024), (2, 512), (4, 64)])
-def test_hotspot_vec_rows_per_thread(gpu, env, rows, block, shuffle):
+def test_hotspot_vec_rows_per_thread(gpu, env, rows, block, shuffle, bx):
     """The vectorised kernel with every rows-per-thread choice and 2-D CTA shapes (row-blocks
-    per CTA), ragged last row chunk and partially idle CTAs included."""
-    env(IB_HOTSPOT_KERNEL="vec", IB_HOTSPOT_VEC_ROWS=rows, IB_HOTSPOT_BLOCK=block, IB_HOTSPOT_SHUFFLE=shuffle)
+    per CTA, CTA width capped at bx threads), ragged last row chunk and partially idle CTAs
+    included."""
+    env(IB_HOTSPOT_KERNEL="vec", IB_HOTSPOT_VEC_ROWS=rows, IB_HOTSPOT_BLOCK=block, IB_HOTSPOT_SHUFFLE=shuffle,
+        IB_HOTSPOT_BX=bx)
     rng = np.random.default_rng(rows)
     # shapes with whole warps per row (the shuffle path: 32 groups of 4/2 cells) and without
     for shape in ((23, 16, 8), (30, 5, 4), (9, 3, 16), (31, 64), (6, 8), (7, 64, 8), (5, 32, 16),
