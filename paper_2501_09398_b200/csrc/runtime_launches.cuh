@@ -262,7 +262,12 @@ inline int lf_threads(const ib_ctx *c, int tj) {  // one thread per (row, 16-byt
   const int64_t groups = c->lat_pitch / (16 / c->esize);
   return (int)(((tj + 1) * groups + 31) / 32 * 32);
 }
-inline LfConfig lf_config(const ib_ctx *c) {
+// short_run: a binary32 H or E launch over <= 40 planes (an axis-0 slab of 256^3 split 8 ways):
+// 3-row tiles with a 4-stage ring, two CTAs per SM, measured best there — 35-plane slab 27.8 vs
+// 32.1 us per H+E iteration (the default shape spends a larger share of a short launch filling
+// its deeper ring), equal at 67 planes and slower beyond (tools/fdtd_slab_tune.py,
+// profiles/r02_slab_scaling.md)
+inline LfConfig lf_config(const ib_ctx *c, bool short_run = false) {
   // The kernel is bound by how much each SM keeps in flight, and the ring depth in planes counts
   // more than its bytes. Measured at 256^3 (us/iter) binary32: TJ=4/NS=6 one CTA per SM 130.7,
   // TJ=4/NS=5 137.3, TJ=3/NS=4 two per SM 138.5, TJ=3/NS=3 196, TJ=4/NS=3 171; binary64 (twice
@@ -273,6 +278,9 @@ inline LfConfig lf_config(const ib_ctx *c) {
   const int es = c->esize;
   const size_t cap = 227 * 1024, half = 113 * 1024;
   const int64_t ftj = env_int("IB_FDTD_TJ", 0), fns = env_int("IB_FDTD_STAGES", 0);
+  if (short_run && ftj <= 0 && fns <= 0 && es == 4 && lf_threads(c, 3) <= ib::kLfNarrowThreads &&
+      lf_smem(3, 4, P, es) <= half)
+    return LfConfig{3, 4, lf_smem(3, 4, P, es)};
   const struct { int tj; bool two; } order[] = {{4, false}, {3, true}, {4, true}, {2, true},
                                                  {3, false}, {2, false}, {1, true}, {1, false}};
   for (int min_ns : {5, 4, 3}) {
@@ -324,7 +332,7 @@ Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int
   const int nx = (int)c->dims[0], ny = (int)c->dims[1], nz = (int)c->dims[2];
   const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
   const bool unit = c->scalars[0] == 1.0;
-  const LfConfig cfg = lf_config(c);
+  const LfConfig cfg = lf_config(c, (mode == ib::kLfH || mode == ib::kLfE) && npl <= 40);
   const int threads = lf_threads(c, cfg.tj);
   const void *fn = lf_fn<T>(unit, cfg.tj, mode, threads > ib::kLfNarrowThreads);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);

@@ -6,7 +6,11 @@ from paper_2501_09398_b200 import workloads as wl
 
 nxs = [int(a) for a in (sys.argv[1:] or ["34", "66"])]
 cfgs = [("auto", {})] + [(f"tj={tj} ch={ch} ns={ns}", {"IB_FDTD_TJ": tj, "IB_FDTD_CHUNKS": ch, "IB_FDTD_STAGES": ns})
-                         for tj in (1, 2, 3, 4) for ch in (1, 2, 3) for ns in (0,)]
+                         for tj in (2, 3, 4) for ch in (1, 2, 3) for ns in (0, 3, 4)]
+if os.environ.get("CFGS"):  # e.g. CFGS="3:3:4,3:2:4" (tj:chunks:stages)
+    cfgs = [("auto", {})] + [(f"tj={a} ch={b} ns={c}", {"IB_FDTD_TJ": int(a), "IB_FDTD_CHUNKS": int(b),
+                                                       "IB_FDTD_STAGES": int(c)})
+                             for a, b, c in (x.split(":") for x in os.environ["CFGS"].split(","))]
 for nx in nxs:
     st = wl.te101_cavity(nx, 256, 256)
     for name, env in cfgs:
