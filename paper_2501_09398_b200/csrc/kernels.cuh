@@ -692,14 +692,6 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
   constexpr int V = 16 / sizeof(T);
   constexpr int ER = TJ + 2, HR = TJ + 1;  // E rows / H rows per stage
   constexpr bool FUSED = MODE == kLfFused || MODE == kLfFusedSlab;
-  // Initial ring fill: only the stages the first plane needs (E_old(i0) and, except for the E
-  // half-step, E_old(i0+1)) are requested up front; the rest follow after that plane's H phase, so
-  // the first data is not queued behind every CTA's whole ring in HBM.
-#ifdef IB_LF_STAGGER
-  constexpr int NFIRST = MODE == kLfE ? 1 : 2;
-#else
-  constexpr int NFIRST = 16;  // everything at once (the ring never exceeds 12 stages)
-#endif
   pdl_trigger();
   T *ring = reinterpret_cast<T *>(smem_raw);
   const int stage = 3 * (ER + HR) * P;  // elements per stage
@@ -765,7 +757,7 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
     __syncthreads();  // every thread is done with the previous run's stages
     if (tid == 0) {
       fence_proxy_async();
-      for (int t = 0; t < min(NFIRST, nload); ++t) issue(t, (int)((g_base + t) % nstages));
+      for (int t = 0; t < min(nstages, nload); ++t) issue(t, (int)((g_base + t) % nstages));
     }
     // stage and mbarrier phase of use g_base + t. binary64: advanced incrementally, no integer
     // division by the run-time ring depth in the plane loop (each costs ~25 uniform instructions
@@ -856,8 +848,6 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
         }
       }
       __syncthreads();  // H_new(i) complete in the ring; plane t-1's stage is free
-      if (NFIRST < 16 && tid == 0 && t == 0)  // the rest of the initial fill (see NFIRST)
-        for (int q = NFIRST; q < min(nstages, nload); ++q) issue(q, (int)((g_base + q) % nstages));
       if (tid == 0 && t >= 1 && t - 1 + nstages < nload) {
         fence_proxy_async();
         issue(t - 1 + nstages, INCR ? sp : (int)((g_base + t - 1 + nstages) % nstages));  // plane t-1's stage
