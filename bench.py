@@ -501,12 +501,17 @@ def measure_e2e(solver, state, cfg, dtype, k, num, pdl, args) -> dict:
     finally:
         for p in ptrs:
             L.ib_host_free(p)
-    return {"value": round(1e6 * statistics.fmean(samples) / n, 4), "unit": UNIT,
+    us = lambda xs: round(1e6 * xs / n, 4)  # noqa: E731
+    # median of the steps: a host wall clock catches the occasional scheduler / page-fault stall of
+    # the box (one 17 ms outlier in 10 calls moved a mean by 40%); mean / min / max kept beside it
+    return {"value": us(statistics.median(samples)), "unit": UNIT, "stat": "median of the steps",
+            "mean": us(statistics.fmean(samples)), "min": us(min(samples)), "max": us(max(samples)),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "call": "workloads.run_batched(program, HotspotWorkload(binary64 arrays), K, I, dtype=%r)" % dtype,
             "note": "host wall clock of the drop-in call: conversion + H2D (pageable) + build + launches + D2H "
                     "+ result dataclass",
-            "pinned": {"value": round(1e6 * statistics.fmean(pinned_samples) / n, 4), "unit": UNIT,
+            "pinned": {"value": us(statistics.median(pinned_samples)), "unit": UNIT,
+                       "mean": us(statistics.fmean(pinned_samples)),
                        "note": "DeviceSolver: pinned H2D of every input field + build + launches + D2H of the "
                                "written fields into a separate pinned buffer"}}
 
