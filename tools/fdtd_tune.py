@@ -6,7 +6,8 @@ from paper_2501_09398_b200 import cli, workloads as wl
 
 n = int(os.environ.get("N", "256"))
 dtype = os.environ.get("DTYPE", "f32")
-st = cli.build_workload("fdtd", [n])
+dims = [int(x) for x in os.environ["DIMS"].split(",")] if os.environ.get("DIMS") else [n]
+st = cli.build_workload("fdtd", dims)
 variants = [("two-kernel staged (default)", False, {}), ("two-kernel lean", False, {"IB_FDTD_KERNEL": "lean"}),
             ("fused default", True, {})]
 shapes = ((4, 3), (4, 4), (4, 5), (4, 6), (3, 4), (3, 7), (3, 8), (2, 8), (2, 10)) if dtype == "f32" else ((4, 3), (3, 4), (2, 3), (2, 4), (2, 5), (2, 6), (1, 6))
