@@ -176,3 +176,33 @@ def test_trace_command_writes_the_measured_model(gpu, capsys, tmp_path, workload
     if kpi == 2:  # one model 'kernel' = one iteration = the H and the E launch
         one = [float(r[0]) for r in rows if r[1] in ("kernel_started", "kernel_ended")]
         assert keys["t_k"] > 0.5 * (one[3] - one[0])
+
+
+# ---- device memory exhaustion -------------------------------------------------------------------
+def test_out_of_device_memory_raises_memory_error_and_leaks_nothing(gpu):
+    """A grid larger than the device (Hotspot3D 4096 x 4096 x 512 binary64: 3 x 68.7 GB) fails
+    ib_create with IB_ENOMEM -> MemoryError (the reference's exception for allocation failure),
+    frees what it had allocated, and the device stays usable."""
+    import ctypes
+
+    from paper_2501_09398_b200 import _lib
+
+    class _Shape:  # shape-only state: no host memory behind it
+        def __init__(self, shape):
+            self.temperature = np.lib.stride_tricks.as_strided(np.zeros(1), shape, [0] * len(shape))
+            self.power = self.temperature
+            self.diffusion_coefficient = 0.1
+
+    wl.release_cached_contexts()
+    L = _lib.lib()
+    free0 = ctypes.c_int64()
+    _lib.check(L.ib_mem_info(0, ctypes.byref(free0), None))
+    with pytest.raises(MemoryError):
+        wl.DeviceSolver(_Shape((4096, 4096, 512)), "f64", upload=False)
+    free1 = ctypes.c_int64()
+    _lib.check(L.ib_mem_info(0, ctypes.byref(free1), None))
+    assert free1.value >= free0.value - (64 << 20)  # nothing left allocated (allocator granularity)
+    state = cli.build_workload("hotspot2d", [64])
+    want = ocpu.hotspot(state.temperature, state.power, state.diffusion_coefficient, 3, np.float64)
+    got = wl.run_batched(wl.hotspot_program(), state, 3, 1).temperature
+    assert np.array_equal(got, want)

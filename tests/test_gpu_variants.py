@@ -344,3 +344,27 @@ def test_fdtd_slabs_equal_one_domain(gpu, env, dims, slabs, dtype):
                 lambda: wl.run_loop(wl.fdtd_program(), state, 6, dtype=dtype, devices=devs, halo="copy")):
         for g, w in zip(run().state_arrays(), want):  # IB_HALO_COPY: peer-copy nodes move the halos
             assert np.array_equal(np.asarray(g, npd), w)
+
+
+def test_fdtd_shallow_staged_shape_takes_lean_kernels(gpu, env):
+    """binary64 rows of 384 cells leave the staged kernel a 1-row tile or a 3-stage ring: the
+    two-half-step solver runs the lean kernels there — still == oracle; forcing
+    IB_FDTD_KERNEL=staged keeps the staged kernel."""
+    base = wl.fdtd_cavity(16, 256, 384)  # 81 MB lattice in binary64: above the L2-resident lean rule
+    rng = np.random.default_rng(11)
+    state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()], base.cell_size,
+                            base.time_step)
+    with wl.DeviceSolver(state, "f64") as s:
+        names = [d["kernel"] for d in s.describe()]
+    assert names and all("k_fdtd_h2" in n or "k_fdtd_e2" in n for n in names), names
+    env(IB_FDTD_KERNEL="staged")
+    with wl.DeviceSolver(state, "f64") as s:
+        assert all("k_fdtd_lf" in d["kernel"] for d in s.describe())
+    dt = state.time_step
+    want = ocpu.fdtd(state.state_arrays(), 1.0, dt / wl.VACUUM_PERMEABILITY, dt / wl.VACUUM_PERMITTIVITY, 2,
+                     np.float64)
+    for kernel in ("staged", "lean"):
+        env(IB_FDTD_KERNEL=kernel)
+        got = wl.run_batched(wl.fdtd_program(), state, 2, 1)
+        for g, w in zip(got.state_arrays(), want):
+            assert np.array_equal(g, w), kernel
