@@ -904,6 +904,125 @@ __global__ void __launch_bounds__(WIDE ? ib::kLfMaxThreads : ib::kLfNarrowThread
   if (fence_sys && halo_stored) peer_fence();
 }
 
+// ================================================================================================
+// FDTD, vectorised lean kernels: the lean kernels' one-launch-per-half-step structure with a
+// 16-byte group of V = 4 floats / 2 doubles of one z row per thread (the staged kernel's per-group
+// arithmetic and masks, its operands loaded straight from the lattice instead of a TMA ring).
+// block = (32 groups along z, 8 along y), grid = (ceil(P / V / 32), ceil((ny + 1) / 8), nx + 1);
+// every lattice cell of the group is written (cells outside a field's extent get 0, as the
+// staged kernel writes them). In place, race free like the scalar lean pair: H reads only E, E
+// reads only H.
+// ================================================================================================
+template <typename T, bool UNIT_D>
+__global__ void __launch_bounds__(256)
+    k_fdtd_h4(T *f, int nx, int ny, int nz, int P, int64_t FS, T c_h, T d) {
+  constexpr int V = 16 / sizeof(T);
+  pdl_trigger();
+  const int k0 = (blockIdx.x * 32 + threadIdx.x) * V;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  const int i = blockIdx.z;
+  pdl_wait();
+  if (k0 >= P || j > ny) return;
+  const int64_t o = ((int64_t)i * (ny + 1) + j) * P + k0, plane = (int64_t)(ny + 1) * P;
+  const T *ex = f, *ey = f + FS, *ez = f + 2 * FS;
+  T *hx = f + 3 * FS, *hy = f + 4 * FS, *hz = f + 5 * FS;
+  const bool ilt = i < nx, jlt = j < ny;
+  T exr[V], eyr[V], ezr[V], hxr[V], hyr[V], hzr[V], exd[V], ezd[V], eyn[V], ezn[V];
+  ld16<T>(hxr, hx + o);
+  ld16<T>(hyr, hy + o);
+  ld16<T>(hzr, hz + o);
+  ld16<T>(exr, ex + o);
+  ld16<T>(eyr, ey + o);
+  ld16<T>(ezr, ez + o);
+  const bool kn = k0 + V < P;
+  const T exk = kn ? ex[o + V] : T(0), eyk = kn ? ey[o + V] : T(0);  // column k0 + V
+  if (jlt) {
+    ld16<T>(exd, ex + o + P);  // row j + 1
+    ld16<T>(ezd, ez + o + P);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) exd[e] = ezd[e] = T(0);
+  }
+  if (ilt) {
+    ld16<T>(eyn, ey + o + plane);  // plane i + 1
+    ld16<T>(ezn, ez + o + plane);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) eyn[e] = ezn[e] = T(0);
+  }
+  T hxo[V], hyo[V], hzo[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) {
+    const int k = k0 + e;
+    const T ey1 = e + 1 < V ? eyr[e + 1] : eyk;  // ey(k+1)
+    const T ex1 = e + 1 < V ? exr[e + 1] : exk;  // ex(k+1)
+    const T a = curl2<T, UNIT_D>(hxr[e], c_h, ey1, eyr[e], ezd[e], ezr[e], d);     // ey(k+1)-ey, ez(j+1)-ez
+    const T b = curl2<T, UNIT_D>(hyr[e], c_h, ezn[e], ezr[e], ex1, exr[e], d);     // ez(i+1)-ez, ex(k+1)-ex
+    const T c = curl2<T, UNIT_D>(hzr[e], c_h, exd[e], exr[e], eyn[e], eyr[e], d);  // ex(j+1)-ex, ey(i+1)-ey
+    hxo[e] = (jlt && k < nz) ? a : T(0);
+    hyo[e] = (ilt && k < nz) ? b : T(0);
+    hzo[e] = (ilt && jlt && k <= nz) ? c : T(0);
+  }
+  st16<T>(hx + o, hxo);
+  st16<T>(hy + o, hyo);
+  st16<T>(hz + o, hzo);
+}
+
+template <typename T, bool UNIT_D>
+__global__ void __launch_bounds__(256)
+    k_fdtd_e4(T *f, int nx, int ny, int nz, int P, int64_t FS, T c_e, T d) {
+  constexpr int V = 16 / sizeof(T);
+  pdl_trigger();
+  const int k0 = (blockIdx.x * 32 + threadIdx.x) * V;
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  const int i = blockIdx.z;
+  pdl_wait();
+  if (k0 >= P || j > ny) return;
+  const int64_t o = ((int64_t)i * (ny + 1) + j) * P + k0, plane = (int64_t)(ny + 1) * P;
+  T *ex = f, *ey = f + FS, *ez = f + 2 * FS;
+  const T *hx = f + 3 * FS, *hy = f + 4 * FS, *hz = f + 5 * FS;
+  const bool ilt = i < nx, iin = i >= 1 && i < nx, jlt = j < ny, jin = j >= 1 && j < ny;
+  T exr[V], eyr[V], ezr[V], hxr[V], hyr[V], hzr[V], hxu[V], hzu[V], hyp[V], hzp[V];
+  ld16<T>(exr, ex + o);
+  ld16<T>(eyr, ey + o);
+  ld16<T>(ezr, ez + o);
+  ld16<T>(hxr, hx + o);
+  ld16<T>(hyr, hy + o);
+  ld16<T>(hzr, hz + o);
+  const T hxm = k0 > 0 ? hx[o - 1] : T(0), hym = k0 > 0 ? hy[o - 1] : T(0);  // column k0 - 1
+  if (j >= 1) {
+    ld16<T>(hxu, hx + o - P);  // row j - 1
+    ld16<T>(hzu, hz + o - P);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) hxu[e] = hzu[e] = T(0);
+  }
+  if (i >= 1) {
+    ld16<T>(hyp, hy + o - plane);  // plane i - 1
+    ld16<T>(hzp, hz + o - plane);
+  } else {
+#pragma unroll
+    for (int e = 0; e < V; ++e) hyp[e] = hzp[e] = T(0);
+  }
+  T exo[V], eyo[V], ezo[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) {
+    const int k = k0 + e;
+    const bool kin = k >= 1 && k < nz;
+    const T hy0 = e > 0 ? hyr[e - 1] : hym;  // hy(k-1)
+    const T hx0 = e > 0 ? hxr[e - 1] : hxm;  // hx(k-1)
+    const T a = curl2<T, UNIT_D>(exr[e], c_e, hzr[e], hzu[e], hyr[e], hy0, d);     // hz(j)-hz(j-1), hy(k)-hy(k-1)
+    const T b = curl2<T, UNIT_D>(eyr[e], c_e, hxr[e], hx0, hzr[e], hzp[e], d);     // hx(k)-hx(k-1), hz(i)-hz(i-1)
+    const T c = curl2<T, UNIT_D>(ezr[e], c_e, hyr[e], hyp[e], hxr[e], hxu[e], d);  // hy(i)-hy(i-1), hx(j)-hx(j-1)
+    exo[e] = (ilt && jin && kin) ? a : T(0);  // walls y in {0,ny}, z in {0,nz}
+    eyo[e] = (jlt && iin && kin) ? b : T(0);  // walls x in {0,nx}, z in {0,nz}
+    ezo[e] = (k < nz && iin && jin) ? c : T(0);  // walls x in {0,nx}, y in {0,ny}
+  }
+  st16<T>(ex + o, exo);
+  st16<T>(ey + o, eyo);
+  st16<T>(ez + o, ezo);
+}
+
 // ---- cross-process halo ordering (peer exchange, runtime.cu: ib_ipc_attach) -------------------------
 // sync[0] = iterations this rank has completed, sync[1] / sync[2] = the up / down neighbour's,
 // written by the neighbour itself through its IPC mapping. Before iteration t's stencil kernel a

@@ -372,8 +372,11 @@ Launch lf_launch(ib_ctx *c, int mode, void *from, void *to, int x0, int npl, int
 template <typename T>
 void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   // The staged kernel marches planes serially per CTA; while the lattice sits in L2 the fully
-  // parallel lean kernels finish sooner (measured us/iter, staged vs lean: 32^3 6.8 / 5.1, 64^3
-  // 8.3 / 7.8, 96^3 17.3 / 15.1, 128^3 28.0 / 28.2, 160^3 66.7 / 71.5). IB_FDTD_KERNEL=lean|staged.
+  // parallel lean kernels finish sooner. Round 2, vectorised lean vs staged (us/iter, binary32 /
+  // binary64, tools/lean_vs_staged.py): 96^3 11.7 / 17.8 and 17.4 / 25.0, 128^3 25.5 / 27.3 and
+  // 54.5 / 48.3 (107 MB lattice), 144^3 33.1 / 44.6, 160^3 56.6 / 62.8, 192^3 94.8 / 89.9, 256^3
+  // 221 / 202 and 385 / 382 — so lean while the lattice is below 104 MB (the hotspot kernels'
+  // L2 crossover too). IB_FDTD_KERNEL=lean|staged.
   // Long z rows leave the staged kernel only 1-row tiles or a 3-stage ring (binary64 384^3: TJ=1 /
   // NS=4 2,508 us/iter, TJ=2 / NS=3 2,042, against 1,408 for the lean kernels: 0.90 of the copy
   // peak; profiles/r02_size_sweep.md, tools/fdtd_tune.py) — the lean kernels take those shapes too.
@@ -383,7 +386,7 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   const bool shallow = cfg.tj <= 1 || cfg.ns <= 3;
   const bool lean = (force && !std::strcmp(force, "lean")) || cfg.tj == 0 ||
                     (!force && shallow && env_int("IB_FDTD_TJ", 0) <= 0 && env_int("IB_FDTD_STAGES", 0) <= 0) ||
-                    (!force && c->slabs.size() == 1 && !c->dist() && lattice_bytes < (40LL << 20));
+                    (!force && c->slabs.size() == 1 && !c->dist() && lattice_bytes < (104LL << 20));
   const int nx = (int)c->dims[0];
   const int P = (int)c->slabs.size();
   if (c->dist()) {  // one rank's slab; the neighbours' halo planes through IPC mappings
@@ -435,9 +438,20 @@ void fdtd_launches(ib_ctx *c, std::vector<Launch> &out) {
   const T d = (T)c->scalars[0], ch = (T)c->scalars[1], ce = (T)c->scalars[2];
   const bool unit = c->scalars[0] == 1.0;
   dim3 b2(32, 8);
-  dim3 grid((unsigned)((nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8), (unsigned)(nx + 1));
-  const void *fh = unit ? (const void *)ib::k_fdtd_h2<T, true> : (const void *)ib::k_fdtd_h2<T, false>;
-  const void *fe = unit ? (const void *)ib::k_fdtd_e2<T, true> : (const void *)ib::k_fdtd_e2<T, false>;
+  // one 16-byte group per thread (k_fdtd_h4 / e4) — measured faster than one cell per thread
+  // (k_fdtd_h2 / e2) wherever HBM matters (us/iter, scalar / vector: binary32 256^3 277 / 224,
+  // 96x256x720 245 / 209, binary64 256^3 432 / 390, 384^3 1379 / 1264), equal on small binary32
+  // grids and 9% slower on small binary64 ones (64^3 8.7 / 9.5), which keep the scalar pair
+  // (tools/lean_ab.py). IB_FDTD_LEANV=0|1 forces one.
+  const int64_t leanv = env_int("IB_FDTD_LEANV", -1);
+  const bool vec = leanv >= 0 ? leanv != 0 : !(c->esize == 8 && lattice_bytes < (32LL << 20));
+  constexpr int V = 16 / sizeof(T);
+  dim3 grid((unsigned)(vec ? (c->lat_pitch / V + 31) / 32 : (nz + 1 + 31) / 32), (unsigned)((ny + 1 + 7) / 8),
+            (unsigned)(nx + 1));
+  const void *fh = vec ? (unit ? (const void *)ib::k_fdtd_h4<T, true> : (const void *)ib::k_fdtd_h4<T, false>)
+                       : (unit ? (const void *)ib::k_fdtd_h2<T, true> : (const void *)ib::k_fdtd_h2<T, false>);
+  const void *fe = vec ? (unit ? (const void *)ib::k_fdtd_e4<T, true> : (const void *)ib::k_fdtd_e4<T, false>)
+                       : (unit ? (const void *)ib::k_fdtd_e2<T, true> : (const void *)ib::k_fdtd_e2<T, false>);
   T *f = (T *)c->lat[0];
   out.push_back(make_launch(fh, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ch, d));
   out.push_back(make_launch(fe, grid, b2, 0, f, nx, ny, nz, (int)c->lat_pitch, c->lat_fs, ce, d));

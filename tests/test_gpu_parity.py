@@ -334,7 +334,7 @@ def test_describe_reports_the_chosen_variants(gpu):
     assert all(k["smem"] > 200 * 1024 for k in f)  # the 6-stage ring
     (ff,) = kernels("fdtd", [256], fuse=True)
     assert "k_fdtd_lf" in ff["kernel"]
-    small = kernels("fdtd", [32])
-    assert [("k_fdtd_h2" in k["kernel"], "k_fdtd_e2" in k["kernel"]) for k in small] == [(True, False), (False, True)]
+    small = kernels("fdtd", [32])  # L2-resident lattice: the vectorised lean pair
+    assert [("k_fdtd_h4" in k["kernel"], "k_fdtd_e4" in k["kernel"]) for k in small] == [(True, False), (False, True)]
     (v,) = kernels("vector", [16384])
     assert "k_vector_f32" in v["kernel"] and v["grid"] == [32, 1, 1]

@@ -175,13 +175,14 @@ FDTD_DIMS = [(8, 4, 8), (5, 6, 7), (1, 1, 1), (3, 1, 9), (16, 9, 33), (2, 40, 3)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("kernel,tj,chunks", [("lean", 0, 0), ("staged", 0, 0), ("staged", 1, 0),
+@pytest.mark.parametrize("kernel,tj,chunks", [("lean", 0, 0), ("lean-scalar", 0, 0), ("staged", 0, 0), ("staged", 1, 0),
                                               ("staged", 2, 3), ("staged", 3, 1), ("staged", 4, 2)])
 @pytest.mark.parametrize("dims", FDTD_DIMS, ids=["x".join(map(str, d)) for d in FDTD_DIMS])
 def test_fdtd_variant_bitwise(gpu, env, dims, kernel, tj, chunks, dtype):
     """The two half-step launches per iteration (in place on the padded lattice): the staged
     k_fdtd_lf H / E modes at every tile height and chunking, and the lean fallback, == oracle."""
-    env(IB_FDTD_KERNEL=kernel, IB_FDTD_TJ=tj, IB_FDTD_CHUNKS=chunks)
+    env(IB_FDTD_KERNEL=kernel.split("-")[0], IB_FDTD_TJ=tj, IB_FDTD_CHUNKS=chunks,
+        IB_FDTD_LEANV=0 if kernel == "lean-scalar" else 1)
     base = wl.fdtd_cavity(*dims)
     rng = np.random.default_rng(sum(dims) + tj + chunks)
     state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()],
@@ -350,13 +351,13 @@ def test_fdtd_shallow_staged_shape_takes_lean_kernels(gpu, env):
     """binary64 rows of 384 cells leave the staged kernel a 1-row tile or a 3-stage ring: the
     two-half-step solver runs the lean kernels there — still == oracle; forcing
     IB_FDTD_KERNEL=staged keeps the staged kernel."""
-    base = wl.fdtd_cavity(16, 256, 384)  # 81 MB lattice in binary64: above the L2-resident lean rule
+    base = wl.fdtd_cavity(48, 256, 384)  # 233 MB lattice in binary64: above the L2-resident lean rule
     rng = np.random.default_rng(11)
     state = wl.FdtdWorkload(*[rng.random(a.shape) for a in base.state_arrays()], base.cell_size,
                             base.time_step)
     with wl.DeviceSolver(state, "f64") as s:
         names = [d["kernel"] for d in s.describe()]
-    assert names and all("k_fdtd_h2" in n or "k_fdtd_e2" in n for n in names), names
+    assert names and all(any(f"k_fdtd_{m}" in n for m in ("h2", "e2", "h4", "e4")) for n in names), names
     env(IB_FDTD_KERNEL="staged")
     with wl.DeviceSolver(state, "f64") as s:
         assert all("k_fdtd_lf" in d["kernel"] for d in s.describe())
