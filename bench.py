@@ -164,19 +164,22 @@ def spawn_ranks(args) -> int:
 # clocks sampler (NVML / nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------------------------
 class Clocks:
-    """SM clock and clock-event reasons sampled DURING a timed region: in-process NVML polling
-    every 200 ms (an nvidia-smi child polling the driver slowed graph instantiation inside the
-    region by milliseconds; each NVML query can still delay a concurrent build by ~0.1 ms, so
-    sparse), nvidia-smi as the fallback. One more sample is taken at the region's end so short
-    regions are covered."""
+    """SM clock and clock-event reasons sampled DURING a timed region: by default one NVML sample
+    after every step (tick(), between steps, so no driver query runs while a step's launches are
+    being issued) plus one at the region's end; the polling-thread mode (between_steps=False) and
+    an nvidia-smi child (when NVML is missing) remain."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, between_steps: bool = True):
         self.device = device
+        # NVML sampled synchronously between steps (tick()), not by a thread polling while the
+        # step's graph launches are being issued: a concurrent driver query is one suspect for
+        # the occasional 25-45% slow timed region on some boxes (profiles/r02_k_sweep.md)
+        self.between_steps = between_steps
         self.proc = None
         self.nvml = None
         self.samples = []  # (sm_mhz, max_mhz, set of reasons)
@@ -215,8 +218,9 @@ class Clocks:
             pynvml.nvmlInit()
             self.nvml = pynvml
             self.handle = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index())
-            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
-            self.thread.start()
+            if not self.between_steps:
+                self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+                self.thread.start()
             return self
         except Exception:
             self.nvml = None
@@ -241,10 +245,19 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def tick(self):
+        """One sample between two steps (NVML mode); a no-op for the nvidia-smi fallback."""
+        if self.nvml is not None and self.between_steps:
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
+
     def __exit__(self, *exc):
         if self.nvml is not None:
             self._stop.set()
-            self.thread.join(timeout=2)
+            if self.thread is not None:
+                self.thread.join(timeout=2)
             try:
                 self._nvml_sample()  # the region's end
                 self.nvml.nvmlShutdown()
@@ -373,6 +386,7 @@ def measure_ours(name, cfg, dtype, args, dist: Dist, device: int, headline: bool
                     solver.upload(state)
                 solver.flush_l2()
                 t = solver.run_batched(k, num, pdl=pdl)
+                clocks.tick()
                 step_s.append(t.gpu_s)
                 tc_s.append(t.build_s)
         solver.sync()
@@ -548,6 +562,7 @@ def measure_dist(name, cfg, dtype, args, dist: Dist) -> dict:
                 s.flush_l2()
                 dist.barrier()
                 steps.append(s.run_batched(k, n // k).gpu_s)
+                clocks.tick()
         step = dist.max(statistics.fmean(steps))
         local_bytes = s.iteration_bytes
         peak, src = measured_peaks()
