@@ -1,5 +1,9 @@
+"""Hotspot2D vectorised-kernel shapes past one wave (diagnostic): rows per thread x CTA size at
+2048^2 / 1536^2 (argv sizes), binary32, graph us/iter (one row per thread past one
+wave).
+    python tools/hotspot2d_shapes.py [N ...]"""
 import os, sys, statistics
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl
 for size in ([int(a)] for a in (sys.argv[1:] or ["2048", "1536"])):
     st = cli.build_workload("hotspot2d", size)

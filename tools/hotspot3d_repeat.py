@@ -1,5 +1,8 @@
+"""Hotspot3D 512^2x8 vectorised-kernel CTA shapes in interleaved repeats (diagnostic): R = 4 in
+128 x 8 CTAs against the alternatives, binary32, graph us/iter.
+    python tools/hotspot3d_repeat.py"""
 import os, sys, statistics
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2501_09398_b200 import cli, workloads as wl
 st = cli.build_workload("hotspot3d", [512, 8])
 cfgs = {"default": {}, "R4 128x8": {"IB_HOTSPOT_VEC_ROWS": "4", "IB_HOTSPOT_BX": "128", "IB_HOTSPOT_BLOCK": "1024"},
