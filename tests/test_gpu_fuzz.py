@@ -1,6 +1,8 @@
 """Randomised shapes, batch sizes and launch options for every solver, bit-exact against the C
 oracle (binary32 and binary64). Seeded: a failure prints its case and reproduces."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -12,8 +14,10 @@ pytestmark = pytest.mark.gpu
 
 
 def _cases(n, seed):
+    """n cases (IB_FUZZ_SCALE multiplies them for a long soak; the seed stays the same, so a
+    failing case reproduces by its index)."""
     rng = np.random.default_rng(seed)
-    for c in range(n):
+    for c in range(n * int(os.environ.get("IB_FUZZ_SCALE", "1"))):
         yield c, rng
 
 
