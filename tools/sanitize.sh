@@ -17,6 +17,7 @@ for tool in memcheck racecheck; do
   KTAG=tma IB_HOTSPOT_KERNEL=tma san $tool hotspot3d 40,16,256 f64; san $tool hotspot3d 24,64,8 f64
   KTAG=scalar IB_HOTSPOT_KERNEL=scalar san $tool hotspot2d 40,128 f32
   san $tool fdtd 9,5,7 f32; san $tool fdtd 20,17,40 f64; KTAG=lean IB_FDTD_KERNEL=lean san $tool fdtd 9,5,7 f32
+  KTAG=lean_scalar IB_FDTD_LEANV=0 IB_FDTD_KERNEL=lean san $tool fdtd 9,5,7 f32; KTAG=leanv IB_FDTD_LEANV=1 IB_FDTD_KERNEL=lean san $tool fdtd 20,17,40 f64
   san $tool fdtd 9,5,7 f32 --fuse; san $tool fdtd 20,17,40 f64 --fuse
   san $tool hotspot3d 30,16,8 f32 "--slabs 3"; san $tool hotspot2d 41,128 f64 "--slabs 2 --halo copy"
   KTAG=tma IB_HOTSPOT_KERNEL=tma san $tool hotspot3d 40,16,256 f32 "--slabs 2"
