@@ -88,7 +88,7 @@ def _worker(rank, world, port, shape, steps, k, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,shape", [(2, (17, 9)), (3, (20, 6, 4)), (2, (5, 3, 8))])
+@pytest.mark.parametrize("world,shape", [(2, (17, 9)), (3, (20, 6, 4)), (2, (5, 3, 8)), (8, (21, 5, 4))])
 def test_gloo_slab_protocol_matches_single_domain(world, shape):
     steps, k = 6, 0.1
     ctx = mp.get_context("spawn")
