@@ -124,7 +124,7 @@ def _rank_main_peer(rank, world, port, shape, kernel, q):
 
 
 @pytest.mark.parametrize("kernel", ["vec", "tma", "scalar"])
-@pytest.mark.parametrize("world,shape", [(2, (64, 24, 8)), (3, (33, 40)), (2, (12, 16, 256))])
+@pytest.mark.parametrize("world,shape", [(2, (64, 24, 8)), (3, (33, 40)), (2, (12, 16, 256)), (8, (40, 24, 8))])
 def test_multi_rank_peer_halo_equals_single_gpu(gpu, kernel, world, shape):
     """One process per rank, halo planes stored straight into the neighbours' buffers (CUDA IPC)
     and ordered by device counters: == the single-domain result, bit for bit. On a one-GPU box
@@ -198,7 +198,7 @@ def _rank_main_fdtd(rank, world, port, dims, dtype, q, fuse=False):
 
 @pytest.mark.parametrize("fuse", [False, True], ids=["two-half-steps", "fused"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("world,dims", [(2, (8, 4, 8)), (3, (16, 9, 33)), (2, (5, 6, 7))])
+@pytest.mark.parametrize("world,dims", [(2, (8, 4, 8)), (3, (16, 9, 33)), (2, (5, 6, 7)), (8, (20, 5, 6))])
 def test_multi_rank_fdtd_peer_equals_single_domain(gpu, world, dims, dtype, fuse):
     """FDTD lattice split into one slab per process, halo planes stored into the neighbours'
     buffers through CUDA IPC with counter ordering (per half-step; per iteration for the fused
